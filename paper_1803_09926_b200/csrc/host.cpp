@@ -1,0 +1,253 @@
+// host.cpp -- the C ABI of include/dwconv.h: validation, kernel-family
+// selection, launch.  No allocation, no synchronisation, no device switch.
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <mutex>
+
+#include <cuda_runtime.h>
+
+#include "../../include/dwconv.h"
+#include "kernels.h"
+
+namespace {
+
+using dwk::ChunkPlan;
+using dwk::Geom;
+
+std::atomic<int> g_override{0};
+
+struct DevInfo {
+  int sms = 0, major = 0, minor = 0, smem_optin = 0;
+  bool ok = false;
+};
+
+// Per-device attribute cache (attributes never change for a device).
+bool dev_info(DevInfo* out) {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  DevInfo& d = cache[dev];
+  if (!d.ok) {
+    if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    d.ok = true;
+  }
+  *out = d;
+  return true;
+}
+
+int out_size(int64_t in, int k, int s, int p, int64_t* o) {
+  const int64_t num = in + 2 * (int64_t)p - k;
+  if (num < 0) return 0;
+  *o = num / s + 1;
+  return 1;
+}
+
+// Validation shared by every entry point.  Fills g on success.
+int validate(const dwconv_desc* d, Geom* g) {
+  if (!d) return DWCONV_ERR_NULL_POINTER;
+  if (d->n < 0 || d->c < 1 || d->h < 1 || d->w < 1) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (d->multiplier < 1 || d->kh < 1 || d->kw < 1 || d->stride_h < 1 || d->stride_w < 1) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (d->pad_h < 0 || d->pad_w < 0) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (d->layout != DWCONV_NCHW && d->layout != DWCONV_NHWC) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (d->dtype != DWCONV_F32 && d->dtype != DWCONV_BF16) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (d->h > INT_MAX || d->w > INT_MAX || d->c > INT_MAX || d->n > INT_MAX) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if ((int64_t)d->kh > d->h + 2 * (int64_t)d->pad_h || (int64_t)d->kw > d->w + 2 * (int64_t)d->pad_w)
+    return DWCONV_ERR_KERNEL_EXCEEDS_INPUT;
+  int64_t ho = 0, wo = 0;
+  if (!out_size(d->h, d->kh, d->stride_h, d->pad_h, &ho) || !out_size(d->w, d->kw, d->stride_w, d->pad_w, &wo) ||
+      ho < 1 || wo < 1)
+    return DWCONV_ERR_KERNEL_EXCEEDS_INPUT;
+  // element counts must stay far from int64 overflow (2^62)
+  const __int128 cm = (__int128)d->c * d->multiplier;
+  const __int128 xs = (__int128)d->n * d->c * d->h * d->w;
+  const __int128 ys = (__int128)d->n * cm * ho * wo;
+  const __int128 ws = cm * d->kh * d->kw;
+  const __int128 lim = (__int128)1 << 62;
+  if (xs > lim || ys > lim || ws > INT_MAX || cm > INT_MAX) return DWCONV_ERR_BAD_DESCRIPTOR;
+  g->N = d->n; g->C = d->c; g->H = d->h; g->W = d->w; g->Ho = ho; g->Wo = wo;
+  g->m = d->multiplier; g->kh = d->kh; g->kw = d->kw; g->sh = d->stride_h; g->sw = d->stride_w;
+  g->ph = d->pad_h; g->pw = d->pad_w; g->layout = d->layout; g->dtype = d->dtype;
+  return DWCONV_OK;
+}
+
+int check_ptr(const void* p, int64_t elems, int eb) {
+  if (elems == 0) return DWCONV_OK;
+  if (!p) return DWCONV_ERR_NULL_POINTER;
+  if (reinterpret_cast<uintptr_t>(p) % (uintptr_t)eb) return DWCONV_ERR_MISALIGNED;
+  return DWCONV_OK;
+}
+
+int check_device(DevInfo* di) {
+  if (!dev_info(di)) return DWCONV_ERR_CUDA;
+  if (di->major != 10) return DWCONV_ERR_UNSUPPORTED;  // built for sm_100a only
+  return DWCONV_OK;
+}
+
+struct Plan {
+  int variant = DWCONV_VARIANT_NONE;
+  ChunkPlan chunk{};
+};
+
+// Choose the kernel family for a pass.  Pure host computation.
+void make_plan(const Geom& g, int pass, const DevInfo& di, Plan* p) {
+  p->variant = DWCONV_VARIANT_GENERIC;
+  if (g.N == 0) { p->variant = DWCONV_VARIANT_NONE; return; }
+  if (g_override.load() == DWCONV_VARIANT_GENERIC) return;
+  if (g.layout == DWCONV_NCHW && dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &p->chunk)) {
+    if (pass != DWCONV_PASS_BWD_FILTER || p->chunk.max_chain <= 160)
+      p->variant = DWCONV_VARIANT_NCHW_CHUNK;
+  }
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? DWCONV_OK : DWCONV_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+int dwconv_abi_version(void) { return DWCONV_ABI_VERSION; }
+
+const char* dwconv_status_string(int s) {
+  switch (s) {
+    case DWCONV_OK: return "ok";
+    case DWCONV_ERR_NULL_POINTER: return "null pointer for a non-empty tensor";
+    case DWCONV_ERR_BAD_DESCRIPTOR: return "bad descriptor";
+    case DWCONV_ERR_KERNEL_EXCEEDS_INPUT: return "kernel exceeds padded input";
+    case DWCONV_ERR_MISALIGNED: return "pointer not aligned to its element size";
+    case DWCONV_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case DWCONV_ERR_UNSUPPORTED: return "unsupported device (needs sm_100)";
+    case DWCONV_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+int dwconv_output_shape(const dwconv_desc* d, int64_t* ho, int64_t* wo) {
+  Geom g;
+  const int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if (!ho || !wo) return DWCONV_ERR_NULL_POINTER;
+  *ho = g.Ho;
+  *wo = g.Wo;
+  return DWCONV_OK;
+}
+
+int dwconv_set_variant_override(int v) {
+  if (v != 0 && v != DWCONV_VARIANT_GENERIC) return DWCONV_ERR_BAD_DESCRIPTOR;
+  g_override.store(v);
+  return DWCONV_OK;
+}
+
+int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwconv_stream stream) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) ||
+      (s = check_ptr(y, g.N * g.C * g.m * g.Ho * g.Wo, eb)))
+    return s;
+  if (g.N == 0) return DWCONV_OK;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  Plan p;
+  make_plan(g, DWCONV_PASS_FWD, di, &p);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
+  return cuda_status(dwk::launch_generic_fwd(g, x, w, y, st));
+}
+
+int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* dx, dwconv_stream stream) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+  if ((s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) || (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) ||
+      (s = check_ptr(dx, g.N * g.C * g.H * g.W, eb)))
+    return s;
+  if (g.N == 0) return DWCONV_OK;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  Plan p;
+  make_plan(g, DWCONV_PASS_BWD_DATA, di, &p);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK)
+    return cuda_status(dwk::launch_nchw_bwd_data(g, p.chunk, dy, w, dx, st));
+  return cuda_status(dwk::launch_generic_bwd_data(g, dy, w, dx, st));
+}
+
+size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
+  Geom g;
+  if (validate(d, &g) != DWCONV_OK) return 0;
+  DevInfo di;
+  if (check_device(&di) != DWCONV_OK) return 0;
+  Plan p;
+  make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
+  return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? p.chunk.ws_bytes : 0;
+}
+
+int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float* dw, void* workspace,
+                      size_t workspace_bytes, dwconv_stream stream) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) ||
+      (s = check_ptr(dw, g.C * g.m * g.kh * g.kw, 4)))
+    return s;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (g.N == 0) return cuda_status(cudaMemsetAsync(dw, 0, (size_t)(g.C * g.m * g.kh * g.kw) * 4, st));
+  Plan p;
+  make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) {
+    if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
+    if (!workspace) return DWCONV_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
+    return cuda_status(dwk::launch_nchw_bwd_filter(g, p.chunk, x, dy, dw, workspace, st));
+  }
+  return cuda_status(dwk::launch_generic_bwd_filter(g, x, dy, dw, st));
+}
+
+int dwconv_workspace_init(void* workspace, size_t workspace_bytes, dwconv_stream stream) {
+  if (workspace_bytes == 0) return DWCONV_OK;
+  if (!workspace) return DWCONV_ERR_NULL_POINTER;
+  return cuda_status(cudaMemsetAsync(workspace, 0, workspace_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if (!info) return DWCONV_ERR_NULL_POINTER;
+  if (pass < 0 || pass > 2) return DWCONV_ERR_BAD_DESCRIPTOR;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  Plan p;
+  make_plan(g, pass, di, &p);
+  std::memset(info, 0, sizeof(*info));
+  info->variant = p.variant;
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) {
+    const ChunkPlan& c = p.chunk;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
+    info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
+    info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+  } else if (p.variant == DWCONV_VARIANT_GENERIC) {
+    info->block = 256; info->launches = 1;
+    if (pass == DWCONV_PASS_BWD_FILTER) {
+      info->grid = (int)(g.C * g.m * g.kh * g.kw);
+      const int64_t per = (g.N * g.Ho * g.Wo + 255) / 256;
+      info->max_chain = (int)(64 + 64 + per / 4096 + 2 + 8);
+    }
+  } else if (pass == DWCONV_PASS_BWD_FILTER) {
+    info->launches = 1;  // memset of dw
+  }
+  return DWCONV_OK;
+}
+
+}  // extern "C"

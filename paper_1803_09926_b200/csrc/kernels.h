@@ -1,0 +1,55 @@
+// kernels.h -- host-visible launch interface between host.cpp and the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dwconv.h"
+
+namespace dwk {
+
+struct FastDiv;
+
+// Geometry shared by every kernel (validated by host.cpp).
+struct Geom {
+  int64_t N, C, H, W, Ho, Wo;
+  int m, kh, kw, sh, sw, ph, pw;
+  int layout, dtype;
+};
+
+// ---- generic kernels (any shape, both layouts): generic.cu
+cudaError_t launch_generic_fwd(const Geom& g, const void* x, const void* w, void* y, cudaStream_t st);
+cudaError_t launch_generic_bwd_data(const Geom& g, const void* dy, const void* w, void* dx, cudaStream_t st);
+cudaError_t launch_generic_bwd_filter(const Geom& g, const void* x, const void* dy, float* dw, cudaStream_t st);
+
+// ---- NCHW chunk kernels: nchw_chunk.cu
+struct ChunkPlan {
+  int threads;          // CTA size
+  int grid;             // CTAs
+  int smem_bytes;       // dynamic smem per CTA (2 stages + barriers)
+  int P;                // input planes per chunk (full-plane mode); 1 in band mode
+  int nbands;           // bands per plane (1 => full-plane mode)
+  int band_rows;        // output rows per band (fwd: y rows, bwd_data: dx rows, bwd_filter: dy rows)
+  int64_t nchunks;      // fwd/bwd_data: chunks iterated by the persistent grid
+  uint32_t in_bytes;    // stage: input buffer bytes (128-aligned)
+  uint32_t in2_bytes;   // stage: second input buffer bytes (bwd_filter dy)
+  uint32_t out_bytes;   // stage: output buffer bytes
+  // bwd_filter only
+  int groups;           // channel groups of P channels
+  int nslices;          // batch slices per group
+  int n_per_slice;      // images per slice
+  int tpg;              // threads per dy plane
+  int max_chain;        // worst-case serial depth of the dw sums
+  size_t ws_bytes;      // workspace
+};
+
+// Returns false if the NCHW chunk family cannot handle the geometry.
+bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan);
+cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
+                            cudaStream_t st);
+cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,
+                                 cudaStream_t st);
+cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
+                                   void* ws, cudaStream_t st);
+
+}  // namespace dwk

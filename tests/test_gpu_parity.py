@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Contract: bitwise on small-integer inputs;
+|gpu - ref| <= 1e-5 * sum|terms| for fp32 random data; bf16 storage adds
+1e-2 * |ref|; dw (always fp32) uses the fp32 rule.  Bitwise run-to-run
+determinism.  Shapes span several chunks/tiles with ragged tails, band mode,
+the generic path, m > 1, K in {3,5,7}, s in {1,2}, both layouts and dtypes.
+"""
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import NCHW, NHWC, check_all, make_inputs, run_gpu, run_oracle, to_dev, check_close
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = [NCHW, NHWC]
+DTYPES = ["f32", "bf16"]
+
+# (N, C, H, W, m, K, s, p)
+CFG1 = (2, 8, 16, 16, 1, 3, 1, 1)
+SHAPES = [
+    CFG1,
+    (3, 5, 13, 11, 1, 3, 2, 1),     # ragged, stride 2, odd sizes
+    (2, 6, 14, 14, 2, 3, 1, 1),     # m = 2, W = 14 (not 16-B rows)
+    (2, 3, 7, 7, 4, 3, 1, 1),       # m = 4, 7x7 planes
+    (2, 4, 12, 10, 1, 5, 1, 2),     # K = 5
+    (1, 3, 15, 9, 1, 7, 1, 3),      # K = 7
+    (2, 3, 17, 12, 1, 5, 2, 2),     # K = 5, s = 2
+    (1, 2, 19, 16, 2, 7, 2, 3),     # K = 7, s = 2, m = 2
+    (2, 3, 80, 80, 1, 3, 1, 1),     # band mode (plane + outputs > stage budget)
+    (2, 2, 96, 72, 1, 3, 2, 1),     # band mode, stride 2
+    (3, 40, 7, 7, 1, 3, 1, 1),      # many small planes, ragged plane groups
+]
+GENERIC_SHAPES = [
+    (2, 3, 9, 11, 1, 2, 3, 0),      # even kernel, stride 3
+    (1, 2, 6, 8, 3, 3, 1, 0),       # m = 3, no padding
+    (2, 3, 8, 9, 1, 3, 2, 2),       # padding larger than (K-1)/2
+]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import paper_1803_09926_b200 as dw
+    dw.dwconv_set_variant_override(0)
+    yield dw
+    dw.dwconv_set_variant_override(0)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("shape", SHAPES + GENERIC_SHAPES)
+def test_parity_random(shape, layout, dtype):
+    check_all(*shape, layout=layout, dtype=dtype, kind="unif")
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("shape", SHAPES + GENERIC_SHAPES)
+def test_parity_integers_bitwise(shape, layout, dtype):
+    amax = 2 if dtype == "bf16" else 3
+    if dtype == "bf16" and shape[5] == 7:
+        amax = 1  # keep |y|, |dx| <= 256 so bf16 stores are exact (SURVEY c.6)
+    check_all(*shape, layout=layout, dtype=dtype, kind="int", amax=amax)
+
+
+@pytest.mark.parametrize("shape", [CFG1, SHAPES[1], SHAPES[8]])
+def test_generic_override_matches_oracle(shape, _lib):
+    _lib.dwconv_set_variant_override(1)
+    try:
+        check_all(*shape, layout=NCHW, dtype="f32", kind="int")
+        check_all(*shape, layout=NCHW, dtype="f32", kind="unif")
+    finally:
+        _lib.dwconv_set_variant_override(0)
+
+
+def test_determinism_bitwise(_lib):
+    inp = make_inputs(4, 32, 56, 56, 1, 3, 1, 1, seed=3)
+    a = run_gpu(inp, 1, 1, NCHW, "f32")
+    b = run_gpu(inp, 1, 1, NCHW, "f32")
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+
+
+def test_workspace_reuse_and_zeroed(_lib):
+    """Two back-to-back bwd_filter calls share one workspace; it is zero afterwards."""
+    import paper_1803_09926_b200.ops as ops
+    inp = make_inputs(8, 16, 28, 28, 1, 3, 2, 1, kind="int", seed=5)
+    x, dy = to_dev(inp["x"], NCHW, "f32"), to_dev(inp["dy"], NCHW, "f32")
+    d = ops.desc_for(x, inp["w"].shape, 2, 1)
+    nbytes = ops.dwconv_bwd_filter_workspace_bytes(d)
+    ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(3):
+        dwt = torch.empty(inp["w"].shape, dtype=torch.float32, device="cuda")
+        ops.dwconv_bwd_filter(d, x, dy, dwt, ws)
+        outs.append(dwt.cpu().numpy())
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+    plan = ops.dwconv_plan(d, 2)
+    assert plan["variant_name"] == "nchw_chunk"
+    assert ws.sum().item() == 0  # tickets and partials are handed back zeroed
+    _, _, (ref, _) = run_oracle(inp, 2, 1)
+    assert np.array_equal(outs[0].astype(np.float64), ref)
+
+
+def test_workspace_shared_across_shapes(_lib):
+    """One workspace buffer serves calls with different plans (group counts) in a row."""
+    import paper_1803_09926_b200.ops as ops
+    shapes = [(2, 3, 80, 80, 1, 3, 1, 1), (3, 40, 7, 7, 1, 3, 1, 1), (2, 8, 16, 16, 1, 3, 1, 1),
+              (4, 64, 14, 14, 1, 3, 2, 1), (3, 40, 7, 7, 1, 3, 1, 1)]
+    ws = torch.zeros(1 << 22, dtype=torch.uint8, device="cuda")
+    for i, sh in enumerate(shapes):
+        N, C, H, W, m, K, s, p = sh
+        inp = make_inputs(*sh, kind="int", seed=20 + i)
+        x, dy = to_dev(inp["x"], NCHW, "f32"), to_dev(inp["dy"], NCHW, "f32")
+        d = ops.desc_for(x, inp["w"].shape, s, p)
+        assert ops.dwconv_bwd_filter_workspace_bytes(d) <= ws.numel()
+        dwt = torch.empty(inp["w"].shape, dtype=torch.float32, device="cuda")
+        ops.dwconv_bwd_filter(d, x, dy, dwt, ws)
+        _, _, (ref, _) = run_oracle(inp, s, p)
+        assert np.array_equal(dwt.cpu().numpy().astype(np.float64), ref), sh
+    assert ws.sum().item() == 0
+
+
+def test_workspace_too_small_errors(_lib):
+    import paper_1803_09926_b200.ops as ops
+    x = torch.zeros(2, 8, 16, 16, device="cuda")
+    dy = torch.zeros(2, 8, 16, 16, device="cuda")
+    d = ops.desc_for(x, (8, 3, 3), 1, 1)
+    need = ops.dwconv_bwd_filter_workspace_bytes(d)
+    assert need > 0
+    dwt = torch.empty(8, 3, 3, device="cuda")
+    with pytest.raises(_lib.DwconvError) as e:
+        ops.dwconv_bwd_filter(d, x, dy, dwt, torch.zeros(need - 16, dtype=torch.uint8, device="cuda"))
+    assert e.value.status == 5
+
+
+def test_empty_batch(_lib):
+    x = torch.zeros(0, 4, 8, 8, device="cuda")
+    w = torch.ones(4, 3, 3, device="cuda")
+    y = _lib.fwd(x, w, 1, 1)
+    assert y.shape == (0, 4, 8, 8)
+    dwt = _lib.bwd_filter(x, torch.zeros(0, 4, 8, 8, device="cuda"), w.shape, 1, 1)
+    torch.cuda.synchronize()
+    assert dwt.shape == (4, 3, 3) and not dwt.any()
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_unaligned_base_pointers(layout, _lib):
+    """Tensors starting 4 bytes past a 16-B boundary take the cooperative-copy path."""
+    N, C, H, W, m, K, s, p = (2, 8, 14, 14, 1, 3, 1, 1)
+    inp = make_inputs(N, C, H, W, m, K, s, p, kind="int", seed=7)
+
+    def shifted(a):
+        flat = torch.zeros(a.size + 1, dtype=torch.float32, device="cuda")
+        t = flat[1:].view(*a.shape)
+        t.copy_(torch.from_numpy(a))
+        assert t.data_ptr() % 16 == 4
+        return t
+
+    x, dy, w = shifted(inp["x"]), shifted(inp["dy"]), to_dev(inp["w"], NCHW, "f32")
+    if layout == NHWC:
+        pytest.skip("channels_last views of an offset buffer are not contiguous views")
+    y = _lib.fwd(x, w, s, p)
+    dx = _lib.bwd_data(dy, w, x.shape, s, p)
+    dwt = _lib.bwd_filter(x, dy, w.shape, s, p)
+    torch.cuda.synchronize()
+    (ry, _), (rdx, _), (rdw, _) = run_oracle(inp, s, p)
+    assert np.array_equal(y.cpu().numpy(), ry) and np.array_equal(dx.cpu().numpy(), rdx)
+    assert np.array_equal(dwt.cpu().numpy(), rdw)
+
+
+def test_autograd_module_matches_oracle(_lib):
+    inp = make_inputs(2, 8, 16, 16, 1, 3, 1, 1, kind="int", seed=9)
+    x = to_dev(inp["x"], NCHW, "f32").requires_grad_(True)
+    mod = _lib.DepthwiseConv2d(8, 3, 1, device="cuda")
+    with torch.no_grad():
+        mod.weight.copy_(torch.from_numpy(inp["w"]).reshape(8, 1, 3, 3))
+    y = mod(x)
+    y.backward(to_dev(inp["dy"], NCHW, "f32"))
+    (ry, _), (rdx, _), (rdw, _) = run_oracle(inp, 1, 1)
+    assert np.array_equal(y.detach().cpu().numpy(), ry)
+    assert np.array_equal(x.grad.cpu().numpy(), rdx)
+    assert np.array_equal(mod.weight.grad.reshape(8, 3, 3).cpu().numpy(), rdw)
+
+
+def test_plan_selects_fast_path_for_mobilenet(_lib):
+    import synth
+    import paper_1803_09926_b200.ops as ops
+    for L in synth.mobilenet_v1_dw(64):
+        d = ops.make_desc(L.n, L.c, L.h, L.w, 1, 3, L.s, 1, NCHW, 0)
+        for pas in (0, 1, 2):
+            info = ops.dwconv_plan(d, pas)
+            assert info["variant_name"] == "nchw_chunk", (L, pas, info)
+            if pas == 2:
+                assert info["max_chain"] <= 160, (L, info)
+
+
+def test_bad_descriptor_errors(_lib):
+    import paper_1803_09926_b200.ops as ops
+    x = torch.zeros(1, 2, 4, 4, device="cuda")
+    w = torch.zeros(2, 5, 5, device="cuda")
+    y = torch.zeros(1, 2, 4, 4, device="cuda")
+    d = ops.make_desc(1, 2, 4, 4, 1, 5, 1, 0)
+    with pytest.raises(_lib.DwconvError) as e:
+        ops.dwconv_fwd(d, x, w, y)
+    assert e.value.status == 3
