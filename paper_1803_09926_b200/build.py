@@ -21,8 +21,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["host.cpp", "generic.cu", "nchw_chunk.cu", "nhwc_tile.cu"]
-HEADERS = ["common.cuh", "kernels.h"]
+SOURCES = ["host.cpp", "generic.cu", "nchw_plan.cu", "nchw_fwd.cu", "nchw_bwd_data.cu", "nchw_bwd_filter.cu",
+           "nhwc_tile.cu"]
+HEADERS = ["common.cuh", "kernels.h", "nchw_common.cuh"]
 
 
 def _deps_mtime() -> float:

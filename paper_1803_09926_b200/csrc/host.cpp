@@ -1,6 +1,8 @@
 // host.cpp -- the C ABI of include/dwconv.h: validation, kernel-family
 // selection, launch.  No allocation, no synchronisation, no device switch.
+#include <array>
 #include <atomic>
+#include <map>
 #include <climits>
 #include <cstring>
 #include <mutex>
@@ -94,8 +96,29 @@ struct Plan {
   ChunkPlan chunk{};
 };
 
-// Choose the kernel family for a pass.  Pure host computation.
+// Choose the kernel family for a pass.  Pure host computation, memoised per
+// (geometry, pass, device, override) because the planner searches many chunkings.
+void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p);
 void make_plan(const Geom& g, int pass, const DevInfo& di, Plan* p) {
+  using Key = std::array<int64_t, 18>;
+  static std::mutex mu;
+  static std::map<Key, Plan> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const Key key = {g.N, g.C, g.H, g.W, g.m, g.kh, g.kw, g.sh, g.sw, g.ph, g.pw, g.layout, g.dtype, pass, dev,
+                   g_override.load(), di.sms, 0};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) { *p = it->second; return; }
+  }
+  make_plan_uncached(g, pass, di, p);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *p;
+}
+
+void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
   p->variant = DWCONV_VARIANT_GENERIC;
   if (g.N == 0) { p->variant = DWCONV_VARIANT_NONE; return; }
   if (g_override.load() == DWCONV_VARIANT_GENERIC) return;

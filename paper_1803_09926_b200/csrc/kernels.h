@@ -26,14 +26,23 @@ cudaError_t launch_generic_bwd_filter(const Geom& g, const void* x, const void* 
 struct ChunkPlan {
   int threads;          // CTA size
   int grid;             // CTAs
-  int smem_bytes;       // dynamic smem per CTA (2 stages + barriers)
+  int smem_bytes;       // dynamic smem per CTA
+  int ri;               // strip-height variant (template index)
+  int R;                // strip height (output rows per thread strip)
+  int vi, V;            // column-vector variant: V = 1 << vi output columns per thread strip
+  int ncg;              // column groups (strips across a row)
+  int nsb;              // strips down a band
   int P;                // input planes per chunk (full-plane mode); 1 in band mode
   int nbands;           // bands per plane (1 => full-plane mode)
   int band_rows;        // output rows per band (fwd: y rows, bwd_data: dx rows, bwd_filter: dy rows)
   int64_t nchunks;      // fwd/bwd_data: chunks iterated by the persistent grid
-  uint32_t in_bytes;    // stage: input buffer bytes (128-aligned)
-  uint32_t in2_bytes;   // stage: second input buffer bytes (bwd_filter dy)
-  uint32_t out_bytes;   // stage: output buffer bytes
+  // shared-memory layout (bytes): barriers | zero row | weights | ns input stages | 2 output stages
+  int ns;                       // input stages (TMA loads in flight = ns - 1)
+  uint32_t zrow_off, w_off;
+  uint32_t in0_off, in_stage;   // first input stage, stride between input stages
+  uint32_t in_bytes;            // input buffer (x / dy) inside a stage, after 128 B of zero slack
+  uint32_t in2_off, in2_bytes;  // bwd_filter: dy buffer inside a stage
+  uint32_t out0_off, out_stage, out_bytes;  // output stages (y / dx)
   // bwd_filter only
   int groups;           // channel groups of P channels
   int nslices;          // batch slices per group

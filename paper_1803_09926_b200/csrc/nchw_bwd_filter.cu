@@ -1,0 +1,284 @@
+// nchw_bwd_filter.cu -- dwconv_bwd_filter for NCHW on sm_100a (see nchw_common.cuh).
+//
+// dw[c*m+j, i, jj] = sum_n sum_{oh,ow} x[n, c, oh*S-PAD+i, ow*S-PAD+jj] * dy[n, c*m+j, oh, ow]
+// -- the block diagonal that Eq. 4 keeps, summed over the
+// batch (reading R5).  CTA = (channel group of P channels, batch slice); groups
+// of `tpg` consecutive threads own one dy plane.  Deterministic reduction:
+//   thread strip (R rows x V cols, fp32 / packed fp32x2 FMA)   chain <= 64
+//   -> running sum over the CTA's chunks                        chain <= 32
+//   -> fixed-order sum over the tpg threads of a plane            <= 32 or tpg/32 + 5
+//   -> per-slice partial in the workspace; the last CTA of the group (integer
+//      ticket) sums the slices pairwise in slice order and re-zeroes the
+//      workspace.                                               depth 2*log2(slices)
+// No float atomics; the worst-case chain is reported by dwconv_plan (max_chain).
+#include "nchw_common.cuh"
+
+namespace dwk {
+namespace nchw {
+namespace {
+
+template <class T, int K, int S, int R, int V>
+__global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a) {
+  constexpr int PAD = (K - 1) / 2, KK = K * K;
+  constexpr int NRows = (R - 1) * S + K;
+  constexpr bool kPacked = (S == 1 && V % 2 == 0);  // float2 accumulators, FFMA2
+  using Wd = Win<K, S, V>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  unsigned* s_last = reinterpret_cast<unsigned*>(smem + 64);
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  const int W = a.W, Wo = a.Wo, m = a.m, H = a.H, Ho = a.Ho;
+  const T* zrow = reinterpret_cast<const T*>(smem + a.zrow_off);
+
+  const int g = blockIdx.x % a.groups;
+  const int sl = blockIdx.x / a.groups;
+  const int c0ch = g * a.P;
+  const int np = min(a.P, (int)(a.C - c0ch));
+  const int64_t n0 = (int64_t)sl * a.nps;
+  const int64_t n1 = min(a.N, n0 + a.nps);
+  const int iters = (int)(n1 - n0) * a.nbands;
+
+  init_bars(bars, a.ns);
+  zero_smem(smem, a);
+  auto sx_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
+  auto sdy_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + a.in2_off + st * a.in_stage); };
+
+  struct Rows { int64_t n; int r0, r1, lo, hi; };
+  auto rows_of = [&](int kk) {
+    Rows r;
+    const int nn = kk / a.nbands;
+    const int b = kk - nn * a.nbands;
+    r.n = n0 + nn;
+    if (a.nbands == 1) { r.r0 = 0; r.r1 = Ho; r.lo = 0; r.hi = H; }
+    else {
+      r.r0 = b * a.BR;
+      r.r1 = min(r.r0 + a.BR, Ho);
+      r.lo = max(0, r.r0 * S - PAD);
+      r.hi = min(H, (r.r1 - 1) * S - PAD + K);
+    }
+    return r;
+  };
+  auto x_src = [&](const Rows& r) { return x + ((r.n * a.C + c0ch) * H + r.lo) * W; };
+  auto x_cnt = [&](const Rows& r) { return (int64_t)np * (r.hi - r.lo) * W; };
+  auto dy_src = [&](const Rows& r, int j) { return dy + (((r.n * a.C + c0ch) * m + j) * Ho + r.r0) * Wo; };
+  auto dy_cnt = [&](const Rows& r) {
+    return (a.nbands == 1) ? (int64_t)np * m * Ho * Wo : (int64_t)(r.r1 - r.r0) * Wo;
+  };
+  auto dy_n = [&]() { return (a.nbands == 1) ? 1 : m; };
+  auto chunk_bulk = [&](const Rows& r) {
+    bool ok = bulk_ok(x_src(r), x_cnt(r), 0);
+    const int64_t dc = dy_cnt(r);
+    for (int j = 0; j < dy_n(); ++j) ok = ok && bulk_ok(dy_src(r, j), dc, (uint32_t)(j * dc * sizeof(T)));
+    return ok;
+  };
+  auto issue = [&](int kk, int st) {
+    const Rows r = rows_of(kk);
+    if (chunk_bulk(r)) {
+      const int64_t xc = x_cnt(r), dc = dy_cnt(r);
+      mbar_arrive_expect_tx(&bars[st], (uint32_t)((xc + dy_n() * dc) * sizeof(T)));
+      bulk_g2s(sx_of(st), x_src(r), (uint32_t)(xc * sizeof(T)), &bars[st]);
+      for (int j = 0; j < dy_n(); ++j)
+        bulk_g2s(sdy_of(st) + j * dc, dy_src(r, j), (uint32_t)(dc * sizeof(T)), &bars[st]);
+    } else {
+      mbar_arrive(&bars[st]);
+    }
+  };
+
+  const int gp = threadIdx.x / a.tpg;  // dy plane of this thread within the group
+  const int lane_g = threadIdx.x - gp * a.tpg;
+  const bool active = gp < np * m;
+  const int ncg = (int)a.div_ncg.d;
+  float run[KK];
+#pragma unroll
+  for (int q = 0; q < KK; ++q) run[q] = 0.f;
+
+  if (threadIdx.x == 0)
+    for (int i = 0; i < a.ns - 1 && i < iters; ++i) issue(i, i);
+  int st = 0;
+  uint32_t par = 0;
+  for (int kk = 0; kk < iters; ++kk) {
+    if (threadIdx.x == 0 && kk + a.ns - 1 < iters) issue(kk + a.ns - 1, st == 0 ? a.ns - 1 : st - 1);
+    const Rows r = rows_of(kk);
+    T* sx = sx_of(st);
+    T* sdy = sdy_of(st);
+    mbar_wait(&bars[st], par);
+    if (++st == a.ns) { st = 0; par ^= 1; }
+    if (!chunk_bulk(r)) {
+      coop_copy(sx, x_src(r), x_cnt(r));
+      const int64_t dc = dy_cnt(r);
+      for (int j = 0; j < dy_n(); ++j) coop_copy(sdy + j * dc, dy_src(r, j), dc);
+    }
+    __syncthreads();
+    if (active) {
+      const int rows_x = r.hi - r.lo;
+      const int rows_dy = r.r1 - r.r0;
+      const T* s_x = sx + ((gp / m) * rows_x - r.lo) * W;  // row ih at s_x + ih * W
+      const T* s_dy = sdy + gp * rows_dy * Wo - r.r0 * Wo;  // row oh at s_dy + oh * Wo
+      float2 loc2[kPacked ? KK : 1];
+      float loc[kPacked ? 1 : KK];
+#pragma unroll
+      for (int q = 0; q < (kPacked ? KK : 1); ++q) loc2[q] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < (kPacked ? 1 : KK); ++q) loc[q] = 0.f;
+      const int ntl = a.nsb * ncg;
+      for (int t = lane_g; t < ntl; t += a.tpg) {
+        const int sb = (int)fdiv((uint32_t)t, a.div_ncg);
+        const int c0 = (t - sb * ncg) * V;
+        const int oh0 = r.r0 + sb * R;
+        float dv[R][V];
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) {
+          if (oh0 + tt < r.r1) {
+            VecIO<T, V>::load(s_dy + (oh0 + tt) * Wo + c0, dv[tt]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < V; ++u) dv[tt][u] = 0.f;
+          }
+        }
+        const int b0 = S * c0;
+        bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+        for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
+#pragma unroll
+        for (int q = 0; q < Wd::NR; ++q) rok[q] = b0 + Wd::NV + q < W;
+        const int ih0 = oh0 * S - PAD;
+#pragma unroll
+        for (int rr = 0; rr < NRows; ++rr) {
+          const int ih = ih0 + rr;
+          const bool rv = (unsigned)(ih - r.lo) < (unsigned)rows_x;
+          const T* p = (rv ? s_x + ih * W : zrow) + b0;
+          float xw[Wd::N];
+          load_window<T, K, S, V>(p, lok, rok, xw);
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt) {
+            const int i = rr - tt * S;
+            if (i >= 0 && i < K) {
+#pragma unroll
+              for (int jj = 0; jj < K; ++jj) {
+                if constexpr (kPacked) {
+#pragma unroll
+                  for (int u = 0; u < V; u += 2)
+                    loc2[i * K + jj] = __ffma2_rn(make_float2(xw[u + jj], xw[u + 1 + jj]),
+                                                  make_float2(dv[tt][u], dv[tt][u + 1]), loc2[i * K + jj]);
+                } else {
+#pragma unroll
+                  for (int u = 0; u < V; ++u) loc[i * K + jj] = fmaf(xw[S * u + jj], dv[tt][u], loc[i * K + jj]);
+                }
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < KK; ++q) run[q] += kPacked ? (loc2[q].x + loc2[q].y) : loc[q];
+    }
+    __syncthreads();  // the stage just consumed is refilled by the next issue
+  }
+
+  // ---- reduce over the tpg threads of each dy plane: every thread parks its sums
+  // in shared memory (the input stages are all consumed), then one warp per
+  // (plane, tap) adds the tpg values -- a strided fixed-order sum per lane and a
+  // fixed shuffle tree across lanes.
+  float* red = reinterpret_cast<float*>(smem + a.in0_off);
+#pragma unroll
+  for (int q = 0; q < KK; ++q) red[threadIdx.x * KK + q] = run[q];
+  __syncthreads();
+  const int Co = a.Co;
+  float* part = a.ws_part + ((int64_t)sl * Co + (int64_t)c0ch * m) * KK;
+  const int nplanes = np * m;
+  if (a.tpg <= 32) {  // one thread per (plane, tap): fixed-order sum of tpg values
+    for (int pq = threadIdx.x; pq < nplanes * KK; pq += (int)blockDim.x) {
+      const int p = pq / KK, q = pq - p * KK;
+      const float* src = red + (p * a.tpg) * KK + q;
+      float v = src[0];
+      for (int u = 1; u < a.tpg; ++u) v += src[u * KK];
+      part[pq] = v;
+    }
+  } else {  // one warp per (plane, tap): strided fixed-order lane sums + shuffle tree
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = (int)(blockDim.x >> 5);
+    for (int pq = warp; pq < nplanes * KK; pq += nwarps) {
+      const int p = pq / KK, q = pq - p * KK;
+      float v = 0.f;
+      for (int u = lane; u < a.tpg; u += 32) v += red[(p * a.tpg + u) * KK + q];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) part[pq] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
+    *s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (*s_last) {
+    __threadfence();
+    const int nvals = np * m * KK;
+    float* base = a.ws_part + (int64_t)c0ch * m * KK;
+    const int64_t sstride = (int64_t)Co * KK;
+    for (int idx = threadIdx.x; idx < nvals; idx += (int)blockDim.x) {
+      // pairwise (binary-counter) summation over slices in slice order; loads
+      // are issued 8 at a time so their latencies overlap.
+      float stk[8];
+      int top = 0;
+      for (int s0 = 0; s0 < a.nslices; s0 += 8) {
+        float vals[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) vals[u] = (s0 + u < a.nslices) ? __ldcg(base + (s0 + u) * sstride + idx) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < a.nslices) __stcg(base + (s0 + u) * sstride + idx, 0.f);  // hand back zero-filled
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int s = s0 + u;
+          if (s < a.nslices) {
+            float cur = vals[u];
+            int bits = s;
+            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+            stk[top++] = cur;
+          }
+        }
+      }
+      float tot = stk[--top];
+      while (top > 0) tot = stk[--top] + tot;
+      a.dw[(int64_t)c0ch * m * KK + idx] = tot;
+    }
+    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;  // leave the workspace zeroed
+  }
+}
+
+template <class T, int K, int S>
+KernelFn pick_rv(int RI, int VI) {
+  constexpr int R0 = rows_bf(K, 0), R1 = rows_bf(K, 1);
+#define DW_V(R)                                                 \
+  switch (VI) {                                                 \
+    case 0: return nchw_bwd_filter_kernel<T, K, S, R, 1>;       \
+    case 1: return nchw_bwd_filter_kernel<T, K, S, R, 2>;       \
+    case 2: return nchw_bwd_filter_kernel<T, K, S, R, 4>;       \
+    default: return nullptr;                                    \
+  }
+  if (RI == 0) { DW_V(R0) } else { DW_V(R1) }
+#undef DW_V
+}
+
+template <class T>
+KernelFn pick_t(int K, int S, int RI, int VI) {
+  if (K == 3 && S == 1) return pick_rv<T, 3, 1>(RI, VI);
+  if (K == 3 && S == 2) return pick_rv<T, 3, 2>(RI, VI);
+  if (K == 5 && S == 1) return pick_rv<T, 5, 1>(RI, VI);
+  if (K == 5 && S == 2) return pick_rv<T, 5, 2>(RI, VI);
+  if (K == 7 && S == 1) return pick_rv<T, 7, 1>(RI, VI);
+  if (K == 7 && S == 2) return pick_rv<T, 7, 2>(RI, VI);
+  return nullptr;
+}
+
+}  // namespace
+
+KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI) {
+  return dtype == DWCONV_F32 ? pick_t<float>(K, S, RI, VI) : pick_t<__nv_bfloat16>(K, S, RI, VI);
+}
+
+}  // namespace nchw
+}  // namespace dwk

@@ -1,0 +1,248 @@
+// nchw_common.cuh -- shared pieces of the NCHW chunk kernels (nchw_fwd.cu,
+// nchw_bwd_data.cu, nchw_bwd_filter.cu) and their planner (nchw_plan.cu).
+//
+// Design: the depthwise layer is a memory-bound stencil
+// (PAPER.md P:62-63).  In NCHW a chunk -- P whole planes, or a band
+// of rows of one large plane plus halo rows -- is one contiguous global range,
+// staged into shared memory by a 1-D TMA bulk copy (cp.async.bulk -> UBLKCP) on
+// an mbarrier, `ns` stages deep.  Each thread computes a strip of R output rows x
+// V adjacent output columns from shared memory with vector loads (LDS.64/128)
+// and, for stride 1, packed fp32x2 FMAs (FFMA2).  Rows outside the staged range
+// read a zero row; the PAD edge columns are predicated loads.  Results leave
+// through a shared-memory tile and a bulk shared->global copy.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dwk {
+namespace nchw {
+
+constexpr int kThreads = 256;  // maximum CTA size (the planner picks <= 256)
+constexpr int kZPad = 8;  // zero-row elements on each side of column 0..W-1
+
+struct NArgs {
+  const void* in;      // fwd: x; bwd_data: dy; bwd_filter: x
+  const void* in2;     // bwd_filter: dy
+  void* out;           // fwd: y; bwd_data: dx
+  const void* w;       // [C*m][K][K] storage dtype
+  float* dw;           // bwd_filter output
+  float* ws_part;      // bwd_filter per-slice partials [nslices][Co][K*K]
+  unsigned* ws_ticket; // bwd_filter tickets [groups]
+  int64_t N, C, Q;     // Q: planes iterated (fwd: N*C x planes, bwd_data: N*C dx planes)
+  int m, Co, H, W, Ho, Wo;
+  int P, nbands, BR, nsb;
+  int64_t nchunks;
+  // shared-memory layout (bytes): [0,128) barriers | zero row | weights |
+  // ns input stages (128 B zero slack | in | 128 B zero slack | in2) | 2 output stages
+  uint32_t zrow_off, w_off;
+  uint32_t in0_off, in_stage, in_bytes, in2_off, in2_bytes;
+  uint32_t out0_off, out_stage, out_bytes;
+  int ns;
+  int groups, nslices, nps, tpg;
+  FastDiv div_ncg, div_nsb, div_m, div_co;
+};
+
+using KernelFn = void (*)(NArgs);
+
+// Kernel tables (one per pass, each in its own translation unit).
+// RI: strip-height variant, VI: column-vector variant (V = 1 << VI).
+KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI);
+KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI);
+KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI);
+
+// Strip heights: index 0 = "7*2^k planes", index 1 = default.
+__host__ __device__ constexpr int rows_fwd(int K, int RI) { return K == 3 ? (RI == 0 ? 7 : 8) : (K == 5 ? 8 : 4); }
+__host__ __device__ constexpr int rows_bd(int K, int S, int RI) {
+  return S == 1 ? rows_fwd(K, RI) : (K == 3 ? (RI == 0 ? 14 : 8) : (K == 5 ? 8 : 4));
+}
+__host__ __device__ constexpr int rows_bf(int K, int RI) { return K == 3 ? (RI == 0 ? 7 : 8) : (K == 5 ? 8 : 4); }
+
+__host__ __device__ constexpr int pmod(int a, int b) { return ((a % b) + b) % b; }
+
+template <class T>
+__device__ __forceinline__ bool bulk_ok(const T* gptr, int64_t count, uint32_t smem_off_bytes) {
+  return ((reinterpret_cast<uintptr_t>(gptr) | (uintptr_t)(count * (int64_t)sizeof(T)) | smem_off_bytes) & 15u) == 0;
+}
+
+struct ChunkRows {
+  int64_t q0;  // first plane of the chunk (fwd/bwd_filter: x plane; bwd_data: dx plane)
+  int np;      // planes in chunk
+  int r0, r1;  // output rows [r0, r1)
+  int lo, hi;  // rows of the input held in smem [lo, hi)
+};
+
+// Zero the zero row and every input stage (with its slack), then order those
+// generic-proxy writes before the first TMA write (fence.proxy.async).
+__device__ __forceinline__ void zero_smem(unsigned char* smem, const NArgs& a) {
+  auto zero = [&](uint32_t off, uint32_t bytes) {
+    uint4* p = reinterpret_cast<uint4*>(smem + off);
+    for (uint32_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+  };
+  zero(a.zrow_off - kZPad * 4, a.w_off - (a.zrow_off - kZPad * 4));
+  zero(a.in0_off, a.ns * a.in_stage);
+  fence_proxy_async_smem();
+  __syncthreads();
+}
+
+__device__ __forceinline__ void init_bars(uint64_t* bars, int ns) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+}
+
+// ------------------------------------------------------------------ vector I/O
+// N consecutive elements at p (aligned to min(16, N * sizeof(T)) bytes) <-> floats.
+template <class T, int N> struct VecIO;
+template <int N> struct VecIO<float, N> {
+  static __device__ __forceinline__ void load(const float* p, float* v) {
+    if constexpr (N == 1) {
+      v[0] = *p;
+    } else if constexpr (N == 2) {
+      const float2 a = *reinterpret_cast<const float2*>(p);
+      v[0] = a.x; v[1] = a.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < N / 4; ++q) {
+        const float4 a = reinterpret_cast<const float4*>(p)[q];
+        v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+      }
+    }
+  }
+  static __device__ __forceinline__ void store(float* p, const float* v) {
+    if constexpr (N == 1) {
+      *p = v[0];
+    } else if constexpr (N == 2) {
+      *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < N / 4; ++q)
+        reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
+};
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t bf_pack(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // round to nearest even
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <int N> struct VecIO<__nv_bfloat16, N> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* v) {
+    if constexpr (N == 1) {
+      v[0] = __bfloat162float(*p);
+    } else if constexpr (N == 2) {
+      const uint32_t a = *reinterpret_cast<const uint32_t*>(p);
+      v[0] = bf_lo(a); v[1] = bf_hi(a);
+    } else if constexpr (N == 4) {
+      const uint2 a = *reinterpret_cast<const uint2*>(p);
+      v[0] = bf_lo(a.x); v[1] = bf_hi(a.x); v[2] = bf_lo(a.y); v[3] = bf_hi(a.y);
+    } else {
+#pragma unroll
+      for (int q = 0; q < N / 8; ++q) {
+        const uint4 a = reinterpret_cast<const uint4*>(p)[q];
+        float* o = v + 8 * q;
+        o[0] = bf_lo(a.x); o[1] = bf_hi(a.x); o[2] = bf_lo(a.y); o[3] = bf_hi(a.y);
+        o[4] = bf_lo(a.z); o[5] = bf_hi(a.z); o[6] = bf_lo(a.w); o[7] = bf_hi(a.w);
+      }
+    }
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* v) {
+    if constexpr (N == 1) {
+      *p = __float2bfloat16_rn(v[0]);
+    } else if constexpr (N == 2) {
+      *reinterpret_cast<uint32_t*>(p) = bf_pack(v[0], v[1]);
+    } else if constexpr (N == 4) {
+      *reinterpret_cast<uint2*>(p) = make_uint2(bf_pack(v[0], v[1]), bf_pack(v[2], v[3]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < N / 8; ++q)
+        reinterpret_cast<uint4*>(p)[q] = make_uint4(bf_pack(v[8 * q], v[8 * q + 1]), bf_pack(v[8 * q + 2], v[8 * q + 3]),
+                                                    bf_pack(v[8 * q + 4], v[8 * q + 5]), bf_pack(v[8 * q + 6], v[8 * q + 7]));
+    }
+  }
+};
+
+// ------------------------------------------------------------------ input window
+// One input row's window for V output columns at stride S: columns
+// [S*c0 - PAD, S*c0 - PAD + (V-1)*S + K).  The S*V columns starting at S*c0 are
+// one aligned vector load; the PAD columns on the left and K-PAD-S on the right
+// are predicated scalar loads (zero outside the plane).
+template <int K, int S, int V>
+struct Win {
+  static constexpr int PAD = (K - 1) / 2;
+  static constexpr int NV = S * V;
+  static constexpr int NL = PAD;
+  static constexpr int NR = (K - PAD - S) > 0 ? (K - PAD - S) : 0;
+  static constexpr int N = NL + NV + NR;
+};
+
+template <class T, int K, int S, int V>
+__device__ __forceinline__ void load_window(const T* p /* at column S*c0 */, const bool* lok, const bool* rok,
+                                            float* xw) {
+  using Wd = Win<K, S, V>;
+  if constexpr (V == 1) {  // V = 1 is the fallback for unaligned rows: scalar loads only
+#pragma unroll
+    for (int q = 0; q < Wd::NV; ++q) xw[Wd::NL + q] = Elem<T>::load(p + q);
+  } else {
+    VecIO<T, Wd::NV>::load(p, xw + Wd::NL);
+  }
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l) xw[l] = lok[l] ? Elem<T>::load(p - Wd::NL + l) : 0.f;
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r) xw[Wd::NL + Wd::NV + r] = rok[r] ? Elem<T>::load(p + Wd::NV + r) : 0.f;
+}
+
+// ------------------------------------------------------------------ stencil strip
+// acc[tt][u] = sum_{i,jj} wr[i*K+jj] * X[oh0*S - PAD + tt*S + i][S*(c0+u) - PAD + jj]
+// where input row ih lives at sp + ih*W when (unsigned)(ih - lo) < rows, else
+// reads the zero row zp.  Used by the forward pass and (with the kernel flipped)
+// the stride-1 input gradient.
+template <class T, int K, int S, int R, int V>
+__device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, int lo, int rows, int ih0, int c0,
+                                              const float* wr, float (&acc)[R][V]) {
+  using Wd = Win<K, S, V>;
+  constexpr int NRows = (R - 1) * S + K;
+  const int b0 = S * c0;
+  bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r) rok[r] = b0 + Wd::NV + r < W;
+#pragma unroll
+  for (int r = 0; r < NRows; ++r) {
+    const int ih = ih0 + r;
+    const bool rv = (unsigned)(ih - lo) < (unsigned)rows;
+    const T* p = (rv ? sp + ih * W : zp) + b0;
+    float xw[Wd::N];
+    load_window<T, K, S, V>(p, lok, rok, xw);
+#pragma unroll
+    for (int tt = 0; tt < R; ++tt) {
+      const int i = r - tt * S;
+      if (i >= 0 && i < K) {
+#pragma unroll
+        for (int jj = 0; jj < K; ++jj) {
+          const float w = wr[i * K + jj];
+          if constexpr (S == 1 && V % 2 == 0) {
+#pragma unroll
+            for (int u = 0; u < V; u += 2) {
+              float2 a = make_float2(acc[tt][u], acc[tt][u + 1]);
+              a = __ffma2_rn(make_float2(w, w), make_float2(xw[u + jj], xw[u + 1 + jj]), a);
+              acc[tt][u] = a.x;
+              acc[tt][u + 1] = a.y;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < V; ++u) acc[tt][u] = fmaf(w, xw[S * u + jj], acc[tt][u]);
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace nchw
+}  // namespace dwk

@@ -1,0 +1,386 @@
+// nchw_plan.cu -- host planner and launchers for the NCHW chunk kernels.
+//
+// For each pass it picks: whole-plane chunks of P planes (or row bands of one
+// plane when a plane does not fit), the strip height R (7 when it divides the
+// plane height, else 8), the column vector V (4/2/1 by row alignment), the TMA
+// ring depth, and for bwd_filter the channel groups x batch slices that fill the
+// GPU while keeping every dw serial chain short (dwconv_plan reports max_chain).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
+#include "nchw_common.cuh"
+
+namespace dwk {
+namespace nchw {
+namespace {
+
+uint32_t round128(uint64_t b) { return (uint32_t)((b + 127) & ~uint64_t(127)); }
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) { int64_t t = a % b; a = b; b = t; }
+  return a;
+}
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  return (v >= lo && v <= hi) ? v : dflt;
+}
+
+int chunk_budget() {  // target bytes of one chunk (input + output)
+  static int kb = env_int("DWCONV_CHUNK_KB", 32, 4, 100);
+  return kb * 1024;
+}
+
+int num_stages() {
+  static int ns = env_int("DWCONV_STAGES", 2, 2, 8);
+  return ns;
+}
+
+int occupancy(KernelFn fn, int smem, int threads) {
+  static std::mutex mu;
+  static KernelFn fns[512] = {};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    bool seen = false;
+    int i = 0;
+    for (; i < 512 && fns[i]; ++i)
+      if (fns[i] == fn) { seen = true; break; }
+    if (!seen && i < 512) {
+      int dev = 0, optin = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      fns[i] = fn;
+    }
+  }
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, smem) != cudaSuccess) return 0;
+  return blocks;
+}
+
+int ilog2_ceil(int64_t v) {
+  int l = 0;
+  while ((1ll << l) < v) ++l;
+  return l;
+}
+
+// Column-vector variant: V = 4, 2 or 1 output columns per thread.  Needs the
+// output width divisible by V and the input rows aligned for the S*V vector load.
+int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb) {
+  for (int vi = 2; vi > 0; --vi) {
+    const int64_t V = 1 << vi;
+    const int64_t align = std::min<int64_t>(16, S * V * eb);
+    if (out_w % V == 0 && (in_w * eb) % align == 0 && (out_w * eb) % std::min<int64_t>(16, V * eb) == 0) return vi;
+  }
+  return 0;
+}
+
+KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI) {
+  if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI);
+  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI);
+  return bwd_filter_kernel(dtype, K, S, RI, VI);
+}
+
+int rows_for(int pass, int K, int S, int RI) {
+  if (pass == DWCONV_PASS_FWD) return rows_fwd(K, RI);
+  if (pass == DWCONV_PASS_BWD_DATA) return rows_bd(K, S, RI);
+  return rows_bf(K, RI);
+}
+
+// Finalise the shared-memory layout of a plan (bytes).
+void layout_smem(ChunkPlan* p, int64_t W, int64_t eb, uint32_t w_bytes, int ns) {
+  p->ns = ns;
+  p->zrow_off = 128 + kZPad * 4;  // element 0 of the zero row (bf16 rows use less of it)
+  const uint32_t zbytes = round128((uint64_t)(W + 2 * kZPad) * (uint64_t)eb + 64);
+  p->w_off = 128 + zbytes;
+  p->in0_off = p->w_off + round128(w_bytes);
+  p->in2_off = 128 + p->in_bytes + 128;  // 128 B of zero slack on both sides of the input buffer
+  p->in_stage = p->in2_off + p->in2_bytes;
+  p->out0_off = p->in0_off + (uint32_t)ns * p->in_stage;
+  p->out_stage = p->out_bytes;
+  p->smem_bytes = (int)(p->out0_off + 2 * p->out_stage);
+}
+
+}  // namespace
+}  // namespace nchw
+
+using nchw::kThreads;
+
+namespace {
+
+// Resident CTAs per SM for a plan, from shared memory and threads (registers are
+// <= 128/thread for every instantiation at 256 threads, so they do not bind first).
+int est_ctas_per_sm(int smem_bytes, int threads) {
+  const int by_smem = (228 * 1024) / (smem_bytes + 1024);
+  const int by_threads = 2048 / threads;
+  return std::max(0, std::min(std::min(by_smem, by_threads), 32));
+}
+
+// Score of a candidate chunking: fraction of issued thread-strip slots doing real
+// work, discounted when chunks are tiny (per-chunk fixed costs) or the SM holds
+// too few warps to hide shared-memory latency.
+double chunk_score(int64_t useful, int64_t slots, int64_t chunk_bytes, int smem, int threads) {
+  const double eff = (double)useful / (double)slots;
+  const double size_f = std::min(1.0, std::sqrt((double)chunk_bytes / (16.0 * 1024)));
+  const int ctas = est_ctas_per_sm(smem, threads);
+  if (ctas < 1) return -1.0;
+  const double warps = (double)ctas * ((threads + 31) / 32);
+  const double occ_f = std::min(1.0, warps / 16.0);
+  return eff * size_f * occ_f;
+}
+
+}  // namespace
+
+bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* p) {
+  using namespace nchw;
+  if (g.layout != DWCONV_NCHW) return false;
+  const int K = g.kh;
+  if (g.kw != K || (K != 3 && K != 5 && K != 7)) return false;
+  const int S = g.sh;
+  if (g.sw != S || (S != 1 && S != 2)) return false;
+  if (g.ph != (K - 1) / 2 || g.pw != (K - 1) / 2) return false;
+  if (g.m < 1 || g.m > 8) return false;
+  if (g.H > 8192 || g.W > 8192 || g.Ho * g.Wo * (int64_t)g.m > (1 << 24)) return false;
+  if (g.N * g.C > (int64_t)1 << 40) return false;
+  // strided windows must stay inside the row (odd W with S = 2 goes to the generic path)
+  if (pass != DWCONV_PASS_BWD_DATA && S * g.Wo > g.W) return false;
+  *p = ChunkPlan{};
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  const int budget = chunk_budget();
+  const int64_t budget_max = std::max<int64_t>(budget, 48 * 1024);
+  const int64_t Q = g.N * g.C;
+  const int m = g.m;
+  const int KK = K * K;
+  const int ns = num_stages();
+  const int64_t x_plane = g.H * g.W * eb;
+  const int64_t y_plane = (int64_t)m * g.Ho * g.Wo * eb;  // the m output planes of one input plane
+  static const int kT[] = {256, 224, 192, 160, 128, 96, 64};
+
+  if (pass == DWCONV_PASS_FWD || pass == DWCONV_PASS_BWD_DATA) {
+    const bool fwd = pass == DWCONV_PASS_FWD;
+    const int64_t in_plane = fwd ? x_plane : y_plane;
+    const int64_t out_plane = fwd ? y_plane : x_plane;
+    const int64_t wpp = (int64_t)m * KK * 4;  // staged weights per input plane
+    const int64_t per = in_plane + out_plane;
+    const int out_rows_total = fwd ? (int)g.Ho : (int)g.H;
+    p->ri = (out_rows_total % rows_for(pass, K, S, 0) == 0) ? 0 : 1;
+    p->R = rows_for(pass, K, S, p->ri);
+    if (fwd) p->vi = pick_vi(g.Wo, g.W, S, eb);
+    else p->vi = (S == 1) ? pick_vi(g.W, g.Wo, 1, eb) : 0;
+    p->V = 1 << p->vi;
+    p->ncg = fwd ? (int)(g.Wo / p->V) : (S == 1 ? (int)(g.W / p->V) : (int)((g.W + S - 1) / S));
+    const int R = p->R;
+    const int nsb_full = (out_rows_total + R - 1) / R;
+    const int64_t tpp = (int64_t)nsb_full * p->ncg;  // thread strips per plane
+    const int64_t a1 = 16 / gcd64(in_plane, 16), a2 = 16 / gcd64(out_plane, 16);
+    const int64_t al = a1 / gcd64(a1, a2) * a2;  // planes per chunk keeping bulk copies 16-B aligned
+    auto in_rows = [&](int br) -> int64_t {
+      if (fwd) return std::min<int64_t>(g.H, (int64_t)(br - 1) * S + K);
+      return std::min<int64_t>(g.Ho, (br + K - 1 + S - 1) / S + 1);
+    };
+    auto band_bytes = [&](int br, int64_t* inb, int64_t* outb) {
+      if (fwd) { *inb = in_rows(br) * g.W * eb; *outb = (int64_t)m * br * g.Wo * eb; }
+      else { *inb = (int64_t)m * in_rows(br) * g.Wo * eb; *outb = (int64_t)br * g.W * eb; }
+    };
+    double best = -1.0;
+    ChunkPlan bestp = *p;
+    auto consider = [&](int T, int P, int nbands, int band_rows, int64_t useful, int64_t slots, int64_t inb,
+                        int64_t outb, int64_t wb) {
+      ChunkPlan c = *p;
+      c.threads = T; c.P = P; c.nbands = nbands; c.band_rows = band_rows;
+      c.in_bytes = round128(inb); c.out_bytes = round128(outb);
+      layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, ns);
+      if (c.smem_bytes > max_smem_optin) layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, 2);
+      if (c.smem_bytes > max_smem_optin) return;
+      const double sc = chunk_score(useful, slots, inb + outb, c.smem_bytes, T);
+      if (sc > best) { best = sc; bestp = c; }
+    };
+    if (per <= budget_max) {  // whole-plane chunks
+      for (int T : kT) {
+        for (int k = 1; k <= 4; ++k) {
+          int64_t P = (int64_t)k * T / tpp;
+          P = std::min<int64_t>(P, 4 * T / (m * KK));  // kernels prefetch <= 4 weights per thread
+          P = std::min<int64_t>(P, budget_max / per);
+          if (P >= al) P = P / al * al;
+          P = std::min<int64_t>(P, Q);
+          if (P < 1 || (P % al != 0 && P != Q)) continue;
+          const int64_t tiles = P * tpp;
+          const int64_t rounds = (tiles + T - 1) / T;
+          // work balance inside a chunk, and across the final partial chunk
+          const int64_t nch = (Q + P - 1) / P;
+          const int64_t useful = Q * tpp;
+          const int64_t slots = nch * rounds * ((T + 31) / 32) * 32;
+          consider(T, (int)P, 1, out_rows_total, useful, slots, P * in_plane, P * out_plane, 2 * P * wpp);
+        }
+      }
+    }
+    if (best < 0.0 || per > budget) {  // row bands of one plane
+      for (int nsb_b = 1; nsb_b <= nsb_full; ++nsb_b) {
+        const int br = nsb_b * R;
+        int64_t inb, outb;
+        band_bytes(br, &inb, &outb);
+        if (inb + outb > budget_max) break;
+        const int nb = (nsb_full + nsb_b - 1) / nsb_b;
+        for (int T : kT) {
+          const int64_t tiles = (int64_t)nsb_b * p->ncg;
+          const int64_t rounds = (tiles + T - 1) / T;
+          const int64_t useful = tpp;
+          const int64_t slots = (int64_t)nb * rounds * ((T + 31) / 32) * 32;
+          consider(T, 1, nb, br, useful, slots, inb, outb, 2 * wpp);
+        }
+      }
+    }
+    if (best < 0.0) return false;
+    *p = bestp;
+    p->nchunks = (p->nbands == 1) ? (Q + p->P - 1) / p->P : Q * p->nbands;
+    p->nsb = (p->band_rows + R - 1) / R;
+    KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi);
+    if (!fn) return false;
+    const int occ = occupancy(fn, p->smem_bytes, p->threads);
+    if (occ < 1) return false;
+    p->grid = (int)std::min<int64_t>(p->nchunks, (int64_t)occ * num_sms);
+    return true;
+  }
+
+  // ---------------- bwd_filter
+  const int64_t per = x_plane + y_plane;
+  p->ri = (g.Ho % rows_bf(K, 0) == 0) ? 0 : 1;
+  p->R = rows_bf(K, p->ri);
+  p->vi = pick_vi(g.Wo, g.W, S, eb);
+  p->V = 1 << p->vi;
+  p->ncg = (int)(g.Wo / p->V);
+  const int R = p->R;
+  const int nsb_full = (int)((g.Ho + R - 1) / R);
+  double best = -1.0;
+  ChunkPlan bestp = *p;
+  auto consider = [&](int P, int tpg, int nb, int br, int64_t xb, int64_t dyb) {
+    const int T = P * m * tpg;
+    if (T > kThreads || T < 64 || T % 32 != 0) return;  // whole warps: the reduction shuffles full warps
+    ChunkPlan c = *p;
+    c.threads = T; c.P = P; c.tpg = tpg; c.nbands = nb; c.band_rows = br;
+    c.in_bytes = round128(xb); c.in2_bytes = round128(dyb); c.out_bytes = 0;
+    layout_smem(&c, g.W, eb, 0, ns);
+    if (c.smem_bytes > max_smem_optin) layout_smem(&c, g.W, eb, 0, 2);
+    // the final reduction parks T * KK floats in the input stages
+    if ((uint32_t)c.ns * c.in_stage < (uint32_t)(T * KK * 4)) {
+      c.in2_bytes += round128(T * KK * 4);
+      layout_smem(&c, g.W, eb, 0, c.ns);
+    }
+    if (c.smem_bytes > max_smem_optin) return;
+    const int nsb_b = (br + R - 1) / R;
+    const int64_t strips = (int64_t)nsb_b * p->ncg;  // per plane per chunk
+    const int64_t rounds = (strips + tpg - 1) / tpg;
+    const int64_t useful = (int64_t)nsb_full * p->ncg * P * m;
+    const int64_t slots = (int64_t)nb * rounds * ((T + 31) / 32) * 32;
+    // fewer channel groups than ~SMs would need many batch slices: discount
+    const int64_t groups = (g.C + P - 1) / P;
+    const double grp_f = std::min(1.0, (double)groups * std::min<int64_t>(g.N, 32) / (2.0 * num_sms));
+    const double sc = chunk_score(useful, slots, xb + dyb, c.smem_bytes, T) * grp_f;
+    if (sc > best) { best = sc; bestp = c; }
+  };
+  if (per <= budget_max) {
+    const int64_t a1 = 16 / gcd64(x_plane, 16), a2 = 16 / gcd64(y_plane, 16);
+    const int64_t al = a1 / gcd64(a1, a2) * a2;
+    for (int P = 1; P * m <= kThreads && P <= g.C && P * per <= budget_max; ++P) {
+      if (P % al != 0 && P != g.C) continue;
+      for (int tpg = 1; P * m * tpg <= kThreads; ++tpg) consider(P, tpg, 1, (int)g.Ho, P * x_plane, P * y_plane);
+    }
+  }
+  if (best < 0.0 || per > budget) {
+    for (int nsb_b = 1; nsb_b <= nsb_full; ++nsb_b) {
+      const int br = nsb_b * R;
+      const int64_t xb = std::min<int64_t>(g.H, (int64_t)(br - 1) * S + K) * g.W * eb;
+      const int64_t dyb = (int64_t)m * br * g.Wo * eb;
+      if (xb + dyb > budget_max) break;
+      const int nb = (nsb_full + nsb_b - 1) / nsb_b;
+      for (int tpg = 1; m * tpg <= kThreads; ++tpg) consider(1, tpg, nb, br, xb, dyb);
+    }
+  }
+  if (best < 0.0) return false;
+  *p = bestp;
+  p->nsb = (p->band_rows + R - 1) / R;
+  p->groups = (int)((g.C + p->P - 1) / p->P);
+  KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi);
+  if (!fn) return false;
+  const int occ = occupancy(fn, p->smem_bytes, p->threads);
+  if (occ < 1) return false;
+  const int nb = p->nbands;
+  // batch slices: ~one wave of CTAs, >= 2 chunks per CTA when the batch allows,
+  // <= 32 chunks per CTA (running-sum chain) and <= 128 slices.
+  const int64_t N = std::max<int64_t>(g.N, 1);
+  int64_t nsl = ((int64_t)num_sms * occ + p->groups - 1) / p->groups;  // ~one wave
+  nsl = std::min<int64_t>(nsl, std::max<int64_t>(1, N * nb / 2));
+  nsl = std::max<int64_t>(nsl, (N * nb + 31) / 32);
+  nsl = std::min<int64_t>(nsl, std::min<int64_t>(N, 128));
+  nsl = std::max<int64_t>(nsl, 1);
+  int64_t nps = (N + nsl - 1) / nsl;
+  nsl = (N + nps - 1) / nps;
+  p->nslices = (int)nsl;
+  p->n_per_slice = (int)nps;
+  p->grid = (int)(p->groups * nsl);
+  p->nchunks = (int64_t)p->grid;
+  const bool packed = (S == 1 && p->V % 2 == 0);
+  const int64_t strips_per_thread = ((int64_t)p->nsb * p->ncg + p->tpg - 1) / p->tpg;
+  const int64_t per_chunk = strips_per_thread * R * (packed ? p->V / 2 : p->V) + (packed ? 1 : 0);
+  const int64_t thread_sum = (p->tpg <= 32) ? p->tpg : (p->tpg + 31) / 32 + 5;
+  p->max_chain = (int)(per_chunk + nps * nb + thread_sum + 2 * ilog2_ceil(nsl) + 1);
+  const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
+  p->ws_bytes = tick + (size_t)nsl * g.C * m * KK * 4;
+  return nsl <= 128;
+}
+
+static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
+  nchw::NArgs a{};
+  a.N = g.N; a.C = g.C; a.Q = g.N * g.C;
+  a.m = g.m; a.Co = (int)(g.C * g.m);
+  a.H = (int)g.H; a.W = (int)g.W; a.Ho = (int)g.Ho; a.Wo = (int)g.Wo;
+  a.P = p.P; a.nbands = p.nbands; a.BR = p.band_rows;
+  a.nsb = p.nsb;
+  a.nchunks = p.nchunks;
+  a.zrow_off = p.zrow_off; a.w_off = p.w_off;
+  a.in0_off = p.in0_off; a.in_stage = p.in_stage; a.in_bytes = p.in_bytes;
+  a.in2_off = p.in2_off; a.in2_bytes = p.in2_bytes;
+  a.out0_off = p.out0_off; a.out_stage = p.out_stage; a.out_bytes = p.out_bytes;
+  a.ns = p.ns;
+  a.groups = p.groups; a.nslices = p.nslices; a.nps = p.n_per_slice; a.tpg = p.tpg;
+  a.div_ncg = make_fastdiv((uint32_t)p.ncg);
+  a.div_nsb = make_fastdiv((uint32_t)p.nsb);
+  a.div_m = make_fastdiv((uint32_t)g.m);
+  a.div_co = make_fastdiv((uint32_t)a.Co);
+  return a;
+}
+
+cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
+                            cudaStream_t st) {
+  nchw::NArgs a = base_args(g, p);
+  a.in = x; a.w = w; a.out = y;
+  nchw::KernelFn fn = nchw::fwd_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi);
+  fn<<<p.grid, p.threads, p.smem_bytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,
+                                 cudaStream_t st) {
+  nchw::NArgs a = base_args(g, p);
+  a.in = dy; a.w = w; a.out = dx;
+  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi);
+  fn<<<p.grid, p.threads, p.smem_bytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
+                                   void* ws, cudaStream_t st) {
+  nchw::NArgs a = base_args(g, p);
+  a.in = x; a.in2 = dy; a.dw = dw;
+  const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
+  a.ws_ticket = static_cast<unsigned*>(ws);
+  a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
+  nchw::KernelFn fn = nchw::bwd_filter_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi);
+  fn<<<p.grid, p.threads, p.smem_bytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dwk
