@@ -106,6 +106,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch: wait until the grids this one depends on have
+// completed and their memory is visible; allow the next grid to start launching.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Cooperative byte copy used when a range is not eligible for a bulk copy
 // (unaligned base or size).  Element granularity is sizeof(T).
 template <class T>

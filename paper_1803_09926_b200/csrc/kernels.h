@@ -30,6 +30,8 @@ struct ChunkPlan {
   int ri;               // strip-height variant (template index)
   int R;                // strip height (output rows per thread strip)
   int vi, V;            // column-vector variant: V = 1 << vi output columns per thread strip
+  bool padded;          // input planes staged with zero rows around them
+  int pitch, zbe;       // padded staging: elements between planes, zero elements above a plane
   int ncg;              // column groups (strips across a row)
   int nsb;              // strips down a band
   int P;                // input planes per chunk (full-plane mode); 1 in band mode

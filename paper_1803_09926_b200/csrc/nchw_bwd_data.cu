@@ -35,7 +35,7 @@ __device__ __forceinline__ ChunkRows bd_rows(const NArgs& a, int64_t c) {
   return k;
 }
 
-template <class T, int K, int S, int R, int V>
+template <class T, int K, int S, int R, int V, bool PADDED>
 __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int kWPT = 4;  // weights per thread per chunk (host keeps P*m*K*K <= 4*256)
@@ -53,8 +53,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) 
   const int W = a.W, Wo = a.Wo, m = a.m, H = a.H;
   const T* zrow = reinterpret_cast<const T*>(smem + a.zrow_off);
 
-  init_bars(bars, a.ns);
-  zero_smem(smem, a);
+  prologue(smem, bars, a);
   auto sin_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
   auto sout_of = [&](int st) { return reinterpret_cast<T*>(smem + a.out0_off + st * a.out_stage); };
   float* sw = reinterpret_cast<float*>(smem + a.w_off);
@@ -84,32 +83,24 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) 
       if (idx < wstride) dst[idx] = wreg[q];
     }
   };
-  if (blockIdx.x < a.nchunks) {
-    load_w(blockIdx.x, wnext);
-    store_w(sw, wnext);
-  }
 
-  // input ranges: whole planes -> one range of np*m planes; band -> m ranges
-  auto in_src = [&](const ChunkRows& k, int j) -> const T* {
-    return dy + ((k.q0 * m + j) * a.Ho + k.lo) * Wo;
-  };
-  auto in_cnt = [&](const ChunkRows& k) -> int64_t {
-    return (a.nbands == 1) ? (int64_t)k.np * m * a.Ho * Wo : (int64_t)(k.hi - k.lo) * Wo;
-  };
-  auto in_n = [&]() { return (a.nbands == 1) ? 1 : m; };
-  auto chunk_bulk = [&](const ChunkRows& k) {
-    const int64_t cnt = in_cnt(k);
-    bool ok = true;
-    for (int j = 0; j < in_n(); ++j) ok = ok && bulk_ok(in_src(k, j), cnt, (uint32_t)(j * cnt * sizeof(T)));
-    return ok;
+  // input staging of a chunk: the m dy planes of each dx plane (rows [lo, hi))
+  auto src_of = [&](const ChunkRows& k) { return dy + ((k.q0 * m) * a.Ho + k.lo) * Wo; };
+  auto spec_of = [&](const ChunkRows& k) {
+    StageSpec sp;
+    sp.cnt = (int64_t)(k.hi - k.lo) * Wo;
+    sp.gstride = (int64_t)a.Ho * Wo;
+    sp.npl = k.np * m;
+    sp.pitch = PADDED ? a.pitch : (int)sp.cnt;
+    sp.zbe = PADDED ? a.zbe : 0;
+    return sp;
   };
   auto issue = [&](int64_t c, int st) {
     const ChunkRows k = bd_rows<K, S>(a, c);
-    const int64_t cnt = in_cnt(k);
-    if (chunk_bulk(k)) {
-      mbar_arrive_expect_tx(&bars[st], (uint32_t)(in_n() * cnt * sizeof(T)));
-      for (int j = 0; j < in_n(); ++j)
-        bulk_g2s(sin_of(st) + j * cnt, in_src(k, j), (uint32_t)(cnt * sizeof(T)), &bars[st]);
+    const StageSpec sp = spec_of(k);
+    if (stage_bulk_ok<T>(src_of(k), sp)) {
+      mbar_arrive_expect_tx(&bars[st], stage_bytes<T>(sp));
+      stage_copy<T>(sin_of(st), src_of(k), sp, &bars[st]);
     } else {
       mbar_arrive(&bars[st]);
     }
@@ -118,6 +109,10 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) 
   if (threadIdx.x == 0)
     for (int i = 0; i < a.ns - 1; ++i)
       if (blockIdx.x + (int64_t)i * gridDim.x < a.nchunks) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
+  if (blockIdx.x < a.nchunks) {  // first chunk's weights (LDG latency overlaps the TMA issue above)
+    load_w(blockIdx.x, wnext);
+    store_w(sw, wnext);
+  }
   int it = 0, st = 0;
   uint32_t par = 0;
   for (int64_t c = blockIdx.x; c < a.nchunks; c += gridDim.x, ++it) {
@@ -134,10 +129,10 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) 
     if (c + gridDim.x < a.nchunks) load_w(c + gridDim.x, wnext);
     mbar_wait(&bars[st], par);
     if (++st == a.ns) { st = 0; par ^= 1; }
-    if (!chunk_bulk(k)) {
-      const int64_t cnt = in_cnt(k);
-      for (int j = 0; j < in_n(); ++j) coop_copy(sin + j * cnt, in_src(k, j), cnt);
-    }
+    const StageSpec sp = spec_of(k);
+    if (!stage_bulk_ok<T>(src_of(k), sp)) stage_coop<T>(sin, src_of(k), sp);
+    if (PADDED && a.nbands > 1 && k.hi == a.Ho)  // zero rows under the last band's dy rows
+      for (int j = 0; j < m; ++j) zero_elems(sin + j * sp.pitch + sp.zbe + sp.cnt, PAD * Wo);
     __syncthreads();
 
     const int rows_dy = k.hi - k.lo;
@@ -166,23 +161,23 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) 
         for (int tt = 0; tt < R; ++tt)
 #pragma unroll
           for (int u = 0; u < TW; ++u) part[tt][u] = 0.f;
-        const T* splane = sin + (pp * m + j) * rows_dy * Wo;
+        const T* splane = sin + (pp * m + j) * sp.pitch + sp.zbe;
         if constexpr (S == 1) {
           // forward stencil with the flipped kernel: dx[ih][iw] = sum wf[a][b] dy[ih-PAD+a][iw-PAD+b]
-          stencil_strip<T, K, 1, R, V>(splane - k.lo * Wo, zrow, Wo, k.lo, rows_dy, ih0 - PAD, iw0, wr, part);
+          stencil_strip<T, K, 1, R, V, PADDED>(splane - k.lo * Wo, zrow, Wo, k.lo, rows_dy, ih0 - PAD, iw0, wr, part);
         } else {
           const int ohb = ih0 / S + D0;
           const int owb = cb + D0;
           bool cok[NCY];
 #pragma unroll
           for (int cy = 0; cy < NCY; ++cy) cok[cy] = (unsigned)(owb + cy) < (unsigned)Wo;
-          const T* sp = splane - k.lo * Wo + owb;
+          const T* spl = splane - k.lo * Wo + owb;
           const T* zp = zrow + owb;
 #pragma unroll
           for (int ry = 0; ry < NRY; ++ry) {
             const int oh = ohb + ry;
-            const bool rok = (unsigned)(oh - k.lo) < (unsigned)rows_dy;
-            const T* p = rok ? sp + oh * Wo : zp;
+            const bool rok = PADDED || (unsigned)(oh - k.lo) < (unsigned)rows_dy;
+            const T* p = rok ? spl + oh * Wo : zp;
             float v[NCY];
 #pragma unroll
             for (int cy = 0; cy < NCY; ++cy) v[cy] = cok[cy] ? Elem<T>::load(p + cy) : 0.f;
@@ -239,43 +234,45 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_data_kernel(const NArgs a) 
     }
     if (threadIdx.x == 0) bulk_commit();
   }
-  if (threadIdx.x == 0) bulk_wait<0>();
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) bulk_wait_read<0>();  // smem must outlive the stores' reads
 }
 
-template <class T, int K, int S>
+template <class T, int K, int S, bool PD>
 KernelFn pick_rv(int RI, int VI) {
   constexpr int R0 = rows_bd(K, S, 0), R1 = rows_bd(K, S, 1);
   if constexpr (S == 1) {
-#define DW_V(R)                                               \
-  switch (VI) {                                               \
-    case 0: return nchw_bwd_data_kernel<T, K, S, R, 1>;       \
-    case 1: return nchw_bwd_data_kernel<T, K, S, R, 2>;       \
-    case 2: return nchw_bwd_data_kernel<T, K, S, R, 4>;       \
-    default: return nullptr;                                  \
+#define DW_V(R)                                                   \
+  switch (VI) {                                                   \
+    case 0: return nchw_bwd_data_kernel<T, K, S, R, 1, PD>;       \
+    case 1: return nchw_bwd_data_kernel<T, K, S, R, 2, PD>;       \
+    case 2: return PD ? nchw_bwd_data_kernel<T, K, S, R, 4, PD> : nullptr; \
+    default: return nullptr;                                      \
   }
     if (RI == 0) { DW_V(R0) } else { DW_V(R1) }
 #undef DW_V
   } else {
     if (VI != 0) return nullptr;
-    return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 1> : nchw_bwd_data_kernel<T, K, S, R1, 1>;
+    return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 1, PD> : nchw_bwd_data_kernel<T, K, S, R1, 1, PD>;
   }
 }
 
-template <class T>
+template <class T, bool PD>
 KernelFn pick_t(int K, int S, int RI, int VI) {
-  if (K == 3 && S == 1) return pick_rv<T, 3, 1>(RI, VI);
-  if (K == 3 && S == 2) return pick_rv<T, 3, 2>(RI, VI);
-  if (K == 5 && S == 1) return pick_rv<T, 5, 1>(RI, VI);
-  if (K == 5 && S == 2) return pick_rv<T, 5, 2>(RI, VI);
-  if (K == 7 && S == 1) return pick_rv<T, 7, 1>(RI, VI);
-  if (K == 7 && S == 2) return pick_rv<T, 7, 2>(RI, VI);
+  if (K == 3 && S == 1) return pick_rv<T, 3, 1, PD>(RI, VI);
+  if (K == 3 && S == 2) return pick_rv<T, 3, 2, PD>(RI, VI);
+  if (K == 5 && S == 1) return pick_rv<T, 5, 1, PD>(RI, VI);
+  if (K == 5 && S == 2) return pick_rv<T, 5, 2, PD>(RI, VI);
+  if (K == 7 && S == 1) return pick_rv<T, 7, 1, PD>(RI, VI);
+  if (K == 7 && S == 2) return pick_rv<T, 7, 2, PD>(RI, VI);
   return nullptr;
 }
 
 }  // namespace
 
-KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI) {
-  return dtype == DWCONV_F32 ? pick_t<float>(K, S, RI, VI) : pick_t<__nv_bfloat16>(K, S, RI, VI);
+KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
+  if (dtype == DWCONV_F32) return padded ? pick_t<float, true>(K, S, RI, VI) : pick_t<float, false>(K, S, RI, VI);
+  return padded ? pick_t<__nv_bfloat16, true>(K, S, RI, VI) : pick_t<__nv_bfloat16, false>(K, S, RI, VI);
 }
 
 }  // namespace nchw

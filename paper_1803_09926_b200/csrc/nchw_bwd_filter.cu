@@ -17,7 +17,7 @@ namespace dwk {
 namespace nchw {
 namespace {
 
-template <class T, int K, int S, int R, int V>
+template <class T, int K, int S, int R, int V, bool PADDED>
 __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int NRows = (R - 1) * S + K;
@@ -39,8 +39,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   const int64_t n1 = min(a.N, n0 + a.nps);
   const int iters = (int)(n1 - n0) * a.nbands;
 
-  init_bars(bars, a.ns);
-  zero_smem(smem, a);
+  prologue(smem, bars, a);
   auto sx_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
   auto sdy_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + a.in2_off + st * a.in_stage); };
 
@@ -60,26 +59,35 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     return r;
   };
   auto x_src = [&](const Rows& r) { return x + ((r.n * a.C + c0ch) * H + r.lo) * W; };
-  auto x_cnt = [&](const Rows& r) { return (int64_t)np * (r.hi - r.lo) * W; };
-  auto dy_src = [&](const Rows& r, int j) { return dy + (((r.n * a.C + c0ch) * m + j) * Ho + r.r0) * Wo; };
-  auto dy_cnt = [&](const Rows& r) {
-    return (a.nbands == 1) ? (int64_t)np * m * Ho * Wo : (int64_t)(r.r1 - r.r0) * Wo;
+  auto dy_src = [&](const Rows& r) { return dy + (((r.n * a.C + c0ch) * m) * Ho + r.r0) * Wo; };
+  auto x_spec = [&](const Rows& r) {
+    StageSpec sp;
+    sp.cnt = (int64_t)(r.hi - r.lo) * W;
+    sp.gstride = (int64_t)H * W;
+    sp.npl = np;
+    sp.pitch = PADDED ? a.pitch : (int)sp.cnt;
+    sp.zbe = PADDED ? a.zbe : 0;
+    return sp;
   };
-  auto dy_n = [&]() { return (a.nbands == 1) ? 1 : m; };
+  auto dy_spec = [&](const Rows& r) {  // dy needs no halo: planes back to back
+    StageSpec sp;
+    sp.cnt = (int64_t)(r.r1 - r.r0) * Wo;
+    sp.gstride = (int64_t)Ho * Wo;
+    sp.npl = np * m;
+    sp.pitch = (int)sp.cnt;
+    sp.zbe = 0;
+    return sp;
+  };
   auto chunk_bulk = [&](const Rows& r) {
-    bool ok = bulk_ok(x_src(r), x_cnt(r), 0);
-    const int64_t dc = dy_cnt(r);
-    for (int j = 0; j < dy_n(); ++j) ok = ok && bulk_ok(dy_src(r, j), dc, (uint32_t)(j * dc * sizeof(T)));
-    return ok;
+    return stage_bulk_ok<T>(x_src(r), x_spec(r)) && stage_bulk_ok<T>(dy_src(r), dy_spec(r));
   };
   auto issue = [&](int kk, int st) {
     const Rows r = rows_of(kk);
     if (chunk_bulk(r)) {
-      const int64_t xc = x_cnt(r), dc = dy_cnt(r);
-      mbar_arrive_expect_tx(&bars[st], (uint32_t)((xc + dy_n() * dc) * sizeof(T)));
-      bulk_g2s(sx_of(st), x_src(r), (uint32_t)(xc * sizeof(T)), &bars[st]);
-      for (int j = 0; j < dy_n(); ++j)
-        bulk_g2s(sdy_of(st) + j * dc, dy_src(r, j), (uint32_t)(dc * sizeof(T)), &bars[st]);
+      const StageSpec xs = x_spec(r), ds = dy_spec(r);
+      mbar_arrive_expect_tx(&bars[st], stage_bytes<T>(xs) + stage_bytes<T>(ds));
+      stage_copy<T>(sx_of(st), x_src(r), xs, &bars[st]);
+      stage_copy<T>(sdy_of(st), dy_src(r), ds, &bars[st]);
     } else {
       mbar_arrive(&bars[st]);
     }
@@ -104,16 +112,17 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     T* sdy = sdy_of(st);
     mbar_wait(&bars[st], par);
     if (++st == a.ns) { st = 0; par ^= 1; }
+    const StageSpec xs = x_spec(r);
     if (!chunk_bulk(r)) {
-      coop_copy(sx, x_src(r), x_cnt(r));
-      const int64_t dc = dy_cnt(r);
-      for (int j = 0; j < dy_n(); ++j) coop_copy(sdy + j * dc, dy_src(r, j), dc);
+      stage_coop<T>(sx, x_src(r), xs);
+      stage_coop<T>(sdy, dy_src(r), dy_spec(r));
     }
+    if (PADDED && a.nbands > 1 && r.hi == H) zero_elems(sx + xs.zbe + xs.cnt, PAD * W);  // rows under the last band
     __syncthreads();
     if (active) {
       const int rows_x = r.hi - r.lo;
       const int rows_dy = r.r1 - r.r0;
-      const T* s_x = sx + ((gp / m) * rows_x - r.lo) * W;  // row ih at s_x + ih * W
+      const T* s_x = sx + (gp / m) * xs.pitch + xs.zbe - r.lo * W;  // row ih at s_x + ih * W
       const T* s_dy = sdy + gp * rows_dy * Wo - r.r0 * Wo;  // row oh at s_dy + oh * Wo
       float2 loc2[kPacked ? KK : 1];
       float loc[kPacked ? 1 : KK];
@@ -146,7 +155,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
 #pragma unroll
         for (int rr = 0; rr < NRows; ++rr) {
           const int ih = ih0 + rr;
-          const bool rv = (unsigned)(ih - r.lo) < (unsigned)rows_x;
+          const bool rv = PADDED || (unsigned)(ih - r.lo) < (unsigned)rows_x;
           const T* p = (rv ? s_x + ih * W : zrow) + b0;
           float xw[Wd::N];
           load_window<T, K, S, V>(p, lok, rok, xw);
@@ -176,6 +185,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     __syncthreads();  // the stage just consumed is refilled by the next issue
   }
 
+  griddep_launch_dependents();
   // ---- reduce over the tpg threads of each dy plane: every thread parks its sums
   // in shared memory (the input stages are all consumed), then one warp per
   // (plane, tap) adds the tpg values -- a strided fixed-order sum per lane and a
@@ -249,35 +259,36 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   }
 }
 
-template <class T, int K, int S>
+template <class T, int K, int S, bool PD>
 KernelFn pick_rv(int RI, int VI) {
   constexpr int R0 = rows_bf(K, 0), R1 = rows_bf(K, 1);
-#define DW_V(R)                                                 \
-  switch (VI) {                                                 \
-    case 0: return nchw_bwd_filter_kernel<T, K, S, R, 1>;       \
-    case 1: return nchw_bwd_filter_kernel<T, K, S, R, 2>;       \
-    case 2: return nchw_bwd_filter_kernel<T, K, S, R, 4>;       \
-    default: return nullptr;                                    \
+#define DW_V(R)                                                     \
+  switch (VI) {                                                     \
+    case 0: return nchw_bwd_filter_kernel<T, K, S, R, 1, PD>;       \
+    case 1: return nchw_bwd_filter_kernel<T, K, S, R, 2, PD>;       \
+    case 2: return PD ? nchw_bwd_filter_kernel<T, K, S, R, 4, PD> : nullptr; \
+    default: return nullptr;                                        \
   }
   if (RI == 0) { DW_V(R0) } else { DW_V(R1) }
 #undef DW_V
 }
 
-template <class T>
+template <class T, bool PD>
 KernelFn pick_t(int K, int S, int RI, int VI) {
-  if (K == 3 && S == 1) return pick_rv<T, 3, 1>(RI, VI);
-  if (K == 3 && S == 2) return pick_rv<T, 3, 2>(RI, VI);
-  if (K == 5 && S == 1) return pick_rv<T, 5, 1>(RI, VI);
-  if (K == 5 && S == 2) return pick_rv<T, 5, 2>(RI, VI);
-  if (K == 7 && S == 1) return pick_rv<T, 7, 1>(RI, VI);
-  if (K == 7 && S == 2) return pick_rv<T, 7, 2>(RI, VI);
+  if (K == 3 && S == 1) return pick_rv<T, 3, 1, PD>(RI, VI);
+  if (K == 3 && S == 2) return pick_rv<T, 3, 2, PD>(RI, VI);
+  if (K == 5 && S == 1) return pick_rv<T, 5, 1, PD>(RI, VI);
+  if (K == 5 && S == 2) return pick_rv<T, 5, 2, PD>(RI, VI);
+  if (K == 7 && S == 1) return pick_rv<T, 7, 1, PD>(RI, VI);
+  if (K == 7 && S == 2) return pick_rv<T, 7, 2, PD>(RI, VI);
   return nullptr;
 }
 
 }  // namespace
 
-KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI) {
-  return dtype == DWCONV_F32 ? pick_t<float>(K, S, RI, VI) : pick_t<__nv_bfloat16>(K, S, RI, VI);
+KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
+  if (dtype == DWCONV_F32) return padded ? pick_t<float, true>(K, S, RI, VI) : pick_t<float, false>(K, S, RI, VI);
+  return padded ? pick_t<__nv_bfloat16, true>(K, S, RI, VI) : pick_t<__nv_bfloat16, false>(K, S, RI, VI);
 }
 
 }  // namespace nchw

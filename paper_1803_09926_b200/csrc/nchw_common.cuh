@@ -40,6 +40,7 @@ struct NArgs {
   uint32_t zrow_off, w_off;
   uint32_t in0_off, in_stage, in_bytes, in2_off, in2_bytes;
   uint32_t out0_off, out_stage, out_bytes;
+  int pitch, zbe;      // PADDED input staging: elements between planes, zero elements above each plane
   int ns;
   int groups, nslices, nps, tpg;
   FastDiv div_ncg, div_nsb, div_m, div_co;
@@ -49,9 +50,10 @@ using KernelFn = void (*)(NArgs);
 
 // Kernel tables (one per pass, each in its own translation unit).
 // RI: strip-height variant, VI: column-vector variant (V = 1 << VI).
-KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI);
-KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI);
-KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI);
+// PADDED: input planes staged with zero rows around them (see stage_issue).
+KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
+KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
+KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
 
 // Strip heights: index 0 = "7*2^k planes", index 1 = default.
 __host__ __device__ constexpr int rows_fwd(int K, int RI) { return K == 3 ? (RI == 0 ? 7 : 8) : (K == 5 ? 8 : 4); }
@@ -74,9 +76,18 @@ struct ChunkRows {
   int lo, hi;  // rows of the input held in smem [lo, hi)
 };
 
-// Zero the zero row and every input stage (with its slack), then order those
-// generic-proxy writes before the first TMA write (fence.proxy.async).
-__device__ __forceinline__ void zero_smem(unsigned char* smem, const NArgs& a) {
+// Kernel prologue shared by the three kernels: thread 0 initialises the ring's
+// mbarriers; all threads zero the zero row and the input stages (padding gaps
+// must read as zero; everything else must at least be finite); the generic-proxy
+// zero writes are ordered before the TMA writes that follow; then the grid waits
+// for the kernels it depends on (programmatic dependent launch).  Kernels call
+// griddep_launch_dependents() once their last chunk is in flight, so the next
+// kernel's launch overlaps this one's tail without taking SM slots early.
+__device__ __forceinline__ void prologue(unsigned char* smem, uint64_t* bars, const NArgs& a) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
   auto zero = [&](uint32_t off, uint32_t bytes) {
     uint4* p = reinterpret_cast<uint4*>(smem + off);
     for (uint32_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
@@ -84,14 +95,8 @@ __device__ __forceinline__ void zero_smem(unsigned char* smem, const NArgs& a) {
   zero(a.zrow_off - kZPad * 4, a.w_off - (a.zrow_off - kZPad * 4));
   zero(a.in0_off, a.ns * a.in_stage);
   fence_proxy_async_smem();
+  griddep_wait();
   __syncthreads();
-}
-
-__device__ __forceinline__ void init_bars(uint64_t* bars, int ns) {
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < ns; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
-  }
 }
 
 // ------------------------------------------------------------------ vector I/O
@@ -196,12 +201,61 @@ __device__ __forceinline__ void load_window(const T* p /* at column S*c0 */, con
   for (int r = 0; r < Wd::NR; ++r) xw[Wd::NL + Wd::NV + r] = rok[r] ? Elem<T>::load(p + Wd::NV + r) : 0.f;
 }
 
+// ------------------------------------------------------------------ input staging
+// A chunk's input is `npl` planes (cnt elements each: rows [lo, hi) of width Wr)
+// whose global data start at src0 + p * gstride.  They land at
+// base + p * pitch + zbe.  With pitch == gstride == cnt and zbe == 0 the planes
+// are back to back and contiguous in global memory: ONE bulk copy.  Otherwise
+// one bulk copy per plane; a PADDED plan leaves zbe zero elements above every
+// plane (and below the last one), so strips need no row checks.
+struct StageSpec {
+  int64_t gstride, cnt;
+  int npl, pitch, zbe;
+};
+template <class T>
+__device__ __forceinline__ bool stage_contig(const StageSpec& s) {
+  return s.gstride == s.cnt && s.pitch == s.cnt && s.zbe == 0;
+}
+template <class T>
+__device__ __forceinline__ bool stage_bulk_ok(const T* src0, const StageSpec& s) {
+  if (stage_contig<T>(s)) return ((reinterpret_cast<uintptr_t>(src0) | (uintptr_t)(s.cnt * s.npl * sizeof(T))) & 15u) == 0;
+  return ((reinterpret_cast<uintptr_t>(src0) | (uintptr_t)(s.gstride * sizeof(T)) | (uintptr_t)(s.cnt * sizeof(T)) |
+           (uintptr_t)(s.pitch * sizeof(T)) | (uintptr_t)(s.zbe * sizeof(T))) & 15u) == 0;
+}
+template <class T>
+__device__ __forceinline__ uint32_t stage_bytes(const StageSpec& s) { return (uint32_t)(s.cnt * s.npl * sizeof(T)); }
+// Thread 0, after the barrier is armed for all bytes: issue the copies.
+template <class T>
+__device__ __forceinline__ void stage_copy(T* base, const T* src0, const StageSpec& s, uint64_t* bar) {
+  if (stage_contig<T>(s)) {
+    bulk_g2s(base, src0, stage_bytes<T>(s), bar);
+  } else {
+    for (int p = 0; p < s.npl; ++p)
+      bulk_g2s(base + p * s.pitch + s.zbe, src0 + p * s.gstride, (uint32_t)(s.cnt * sizeof(T)), bar);
+  }
+}
+// All threads: cooperative copy (used when the stage was not bulk-eligible).
+template <class T>
+__device__ __forceinline__ void stage_coop(T* base, const T* src0, const StageSpec& s) {
+  if (stage_contig<T>(s)) {
+    coop_copy(base, src0, s.cnt * s.npl);
+  } else {
+    for (int p = 0; p < s.npl; ++p) coop_copy(base + p * s.pitch + s.zbe, src0 + p * s.gstride, s.cnt);
+  }
+}
+// All threads: write zeros to n elements (band-mode bottom padding rows).
+template <class T>
+__device__ __forceinline__ void zero_elems(T* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = T(0.f);
+}
+
 // ------------------------------------------------------------------ stencil strip
 // acc[tt][u] = sum_{i,jj} wr[i*K+jj] * X[oh0*S - PAD + tt*S + i][S*(c0+u) - PAD + jj]
-// where input row ih lives at sp + ih*W when (unsigned)(ih - lo) < rows, else
-// reads the zero row zp.  Used by the forward pass and (with the kernel flipped)
-// the stride-1 input gradient.
-template <class T, int K, int S, int R, int V>
+// where input row ih lives at sp + ih*W.  PADDED: every row the strip touches is
+// staged or a zero row.  DENSE: rows with (unsigned)(ih - lo) >= rows read the
+// zero row zp.  Used by the forward pass and (with the kernel flipped) the
+// stride-1 input gradient.
+template <class T, int K, int S, int R, int V, bool PADDED>
 __device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, int lo, int rows, int ih0, int c0,
                                               const float* wr, float (&acc)[R][V]) {
   using Wd = Win<K, S, V>;
@@ -212,11 +266,17 @@ __device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, i
   for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
 #pragma unroll
   for (int r = 0; r < Wd::NR; ++r) rok[r] = b0 + Wd::NV + r < W;
+  const T* prow = sp + ih0 * W + b0;
 #pragma unroll
   for (int r = 0; r < NRows; ++r) {
-    const int ih = ih0 + r;
-    const bool rv = (unsigned)(ih - lo) < (unsigned)rows;
-    const T* p = (rv ? sp + ih * W : zp) + b0;
+    const T* p;
+    if constexpr (PADDED) {
+      p = prow + r * W;
+    } else {
+      const int ih = ih0 + r;
+      const bool rv = (unsigned)(ih - lo) < (unsigned)rows;
+      p = rv ? prow + r * W : zp + b0;
+    }
     float xw[Wd::N];
     load_window<T, K, S, V>(p, lok, rok, xw);
 #pragma unroll

@@ -30,7 +30,7 @@ __device__ __forceinline__ ChunkRows fwd_rows(const NArgs& a, int64_t c) {
   return k;
 }
 
-template <class T, int K, int S, int R, int V>
+template <class T, int K, int S, int R, int V, bool PADDED>
 __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int kWPT = 4;  // weights per thread per chunk (host keeps P*m*K*K <= 4*256)
@@ -42,8 +42,7 @@ __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
   const int W = a.W, Wo = a.Wo, m = a.m;
   const T* zrow = reinterpret_cast<const T*>(smem + a.zrow_off);
 
-  init_bars(bars, a.ns);
-  zero_smem(smem, a);
+  prologue(smem, bars, a);
   auto sin_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
   auto sout_of = [&](int st) { return reinterpret_cast<T*>(smem + a.out0_off + st * a.out_stage); };
   float* sw = reinterpret_cast<float*>(smem + a.w_off);
@@ -73,18 +72,24 @@ __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
       if (idx < wstride) dst[idx] = wreg[q];
     }
   };
-  if (blockIdx.x < a.nchunks) {
-    load_w(blockIdx.x, wnext);
-    store_w(sw, wnext);
-  }
 
+  // input staging of a chunk: its x planes (rows [lo, hi) of each)
+  auto spec_of = [&](const ChunkRows& k) {
+    StageSpec sp;
+    sp.cnt = (int64_t)(k.hi - k.lo) * W;
+    sp.gstride = (int64_t)a.H * W;
+    sp.npl = k.np;
+    sp.pitch = PADDED ? a.pitch : (int)sp.cnt;
+    sp.zbe = PADDED ? a.zbe : 0;
+    return sp;
+  };
   auto issue = [&](int64_t c, int st) {  // thread 0
     const ChunkRows k = fwd_rows<K, S>(a, c);
     const T* src = x + (k.q0 * a.H + k.lo) * W;
-    const int64_t cnt = (int64_t)k.np * (k.hi - k.lo) * W;
-    if (bulk_ok(src, cnt, 0)) {
-      mbar_arrive_expect_tx(&bars[st], (uint32_t)(cnt * sizeof(T)));
-      bulk_g2s(sin_of(st), src, (uint32_t)(cnt * sizeof(T)), &bars[st]);
+    const StageSpec sp = spec_of(k);
+    if (stage_bulk_ok<T>(src, sp)) {
+      mbar_arrive_expect_tx(&bars[st], stage_bytes<T>(sp));
+      stage_copy<T>(sin_of(st), src, sp, &bars[st]);
     } else {
       mbar_arrive(&bars[st]);
     }
@@ -93,6 +98,10 @@ __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
   if (threadIdx.x == 0)
     for (int i = 0; i < a.ns - 1; ++i)
       if (blockIdx.x + (int64_t)i * gridDim.x < a.nchunks) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
+  if (blockIdx.x < a.nchunks) {  // first chunk's weights (LDG latency overlaps the TMA issue above)
+    load_w(blockIdx.x, wnext);
+    store_w(sw, wnext);
+  }
   int it = 0, st = 0;
   uint32_t par = 0;
   for (int64_t c = blockIdx.x; c < a.nchunks; c += gridDim.x, ++it) {
@@ -110,14 +119,17 @@ __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
     if (c + gridDim.x < a.nchunks) load_w(c + gridDim.x, wnext);
     mbar_wait(&bars[st], par);
     if (++st == a.ns) { st = 0; par ^= 1; }
+    const StageSpec sp = spec_of(k);
     {
       const T* src = x + (k.q0 * a.H + k.lo) * W;
-      const int64_t cnt = (int64_t)k.np * (k.hi - k.lo) * W;
-      if (!bulk_ok(src, cnt, 0)) coop_copy(sin, src, cnt);
+      if (!stage_bulk_ok<T>(src, sp)) stage_coop<T>(sin, src, sp);
+      // band mode: the padding rows under the last band are zero rows
+      if (PADDED && a.nbands > 1 && k.hi == a.H) zero_elems(sin + sp.zbe + sp.cnt, PAD * W);
     }
     __syncthreads();
 
     const int rows_in = k.hi - k.lo;
+    (void)rows_in;
     const int rows_out = k.r1 - k.r0;
     const int ncg = (int)a.div_ncg.d;
     const int ntiles = npl * a.nsb * ncg;
@@ -136,8 +148,8 @@ __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
       for (int tt = 0; tt < R; ++tt)
 #pragma unroll
         for (int u = 0; u < V; ++u) acc[tt][u] = 0.f;
-      stencil_strip<T, K, S, R, V>(sin + (pin * rows_in - k.lo) * W, zrow, W, k.lo, rows_in, oh0 * S - PAD, c0, wr,
-                                   acc);
+      stencil_strip<T, K, S, R, V, PADDED>(sin + pin * sp.pitch + sp.zbe - k.lo * W, zrow, W, k.lo, rows_in,
+                                           oh0 * S - PAD, c0, wr, acc);
       T* so = sout + (pp * rows_out + (oh0 - k.r0)) * Wo + c0;
 #pragma unroll
       for (int tt = 0; tt < R; ++tt)
@@ -166,38 +178,40 @@ __global__ void __launch_bounds__(kThreads) nchw_fwd_kernel(const NArgs a) {
     }
     if (threadIdx.x == 0) bulk_commit();
   }
-  if (threadIdx.x == 0) bulk_wait<0>();
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) bulk_wait_read<0>();  // smem must outlive the stores' reads
 }
 
-template <class T, int K, int S>
+template <class T, int K, int S, bool PD>
 KernelFn pick_rv(int RI, int VI) {
   constexpr int R0 = rows_fwd(K, 0), R1 = rows_fwd(K, 1);
-#define DW_V(R)                                          \
-  switch (VI) {                                          \
-    case 0: return nchw_fwd_kernel<T, K, S, R, 1>;       \
-    case 1: return nchw_fwd_kernel<T, K, S, R, 2>;       \
-    case 2: return nchw_fwd_kernel<T, K, S, R, 4>;       \
-    default: return nullptr;                             \
+#define DW_V(R)                                              \
+  switch (VI) {                                              \
+    case 0: return nchw_fwd_kernel<T, K, S, R, 1, PD>;       \
+    case 1: return nchw_fwd_kernel<T, K, S, R, 2, PD>;       \
+    case 2: return PD ? nchw_fwd_kernel<T, K, S, R, 4, PD> : nullptr; \
+    default: return nullptr;                                 \
   }
   if (RI == 0) { DW_V(R0) } else { DW_V(R1) }
 #undef DW_V
 }
 
-template <class T>
+template <class T, bool PD>
 KernelFn pick_t(int K, int S, int RI, int VI) {
-  if (K == 3 && S == 1) return pick_rv<T, 3, 1>(RI, VI);
-  if (K == 3 && S == 2) return pick_rv<T, 3, 2>(RI, VI);
-  if (K == 5 && S == 1) return pick_rv<T, 5, 1>(RI, VI);
-  if (K == 5 && S == 2) return pick_rv<T, 5, 2>(RI, VI);
-  if (K == 7 && S == 1) return pick_rv<T, 7, 1>(RI, VI);
-  if (K == 7 && S == 2) return pick_rv<T, 7, 2>(RI, VI);
+  if (K == 3 && S == 1) return pick_rv<T, 3, 1, PD>(RI, VI);
+  if (K == 3 && S == 2) return pick_rv<T, 3, 2, PD>(RI, VI);
+  if (K == 5 && S == 1) return pick_rv<T, 5, 1, PD>(RI, VI);
+  if (K == 5 && S == 2) return pick_rv<T, 5, 2, PD>(RI, VI);
+  if (K == 7 && S == 1) return pick_rv<T, 7, 1, PD>(RI, VI);
+  if (K == 7 && S == 2) return pick_rv<T, 7, 2, PD>(RI, VI);
   return nullptr;
 }
 
 }  // namespace
 
-KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI) {
-  return dtype == DWCONV_F32 ? pick_t<float>(K, S, RI, VI) : pick_t<__nv_bfloat16>(K, S, RI, VI);
+KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
+  if (dtype == DWCONV_F32) return padded ? pick_t<float, true>(K, S, RI, VI) : pick_t<float, false>(K, S, RI, VI);
+  return padded ? pick_t<__nv_bfloat16, true>(K, S, RI, VI) : pick_t<__nv_bfloat16, false>(K, S, RI, VI);
 }
 
 }  // namespace nchw

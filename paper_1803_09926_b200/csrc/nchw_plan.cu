@@ -78,11 +78,13 @@ int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb) {
   return 0;
 }
 
-KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI) {
-  if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI);
-  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI);
-  return bwd_filter_kernel(dtype, K, S, RI, VI);
+KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded) {
+  if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI, padded);
+  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded);
+  return bwd_filter_kernel(dtype, K, S, RI, VI, padded);
 }
+
+int64_t round16(int64_t b) { return (b + 15) & ~int64_t(15); }
 
 int rows_for(int pass, int K, int S, int RI) {
   if (pass == DWCONV_PASS_FWD) return rows_fwd(K, RI);
@@ -165,6 +167,13 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     const int64_t out_plane = fwd ? y_plane : x_plane;
     const int64_t wpp = (int64_t)m * KK * 4;  // staged weights per input plane
     const int64_t per = in_plane + out_plane;
+    const int PADr = (K - 1) / 2;
+    const int64_t Win = fwd ? g.W : g.Wo, Hin = fwd ? g.H : g.Ho;
+    const int64_t npi = fwd ? 1 : m;  // staged input planes per chunk plane
+    const int64_t zbe_b = round16(PADr * Win * eb);
+    // padded staging needs 16-B aligned planes (full mode) or rows (band mode)
+    const bool pad_full = (Hin * Win * eb) % 16 == 0;
+    const bool pad_band = (Win * eb) % 16 == 0;
     const int out_rows_total = fwd ? (int)g.Ho : (int)g.H;
     p->ri = (out_rows_total % rows_for(pass, K, S, 0) == 0) ? 0 : 1;
     p->R = rows_for(pass, K, S, p->ri);
@@ -213,7 +222,13 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
           const int64_t nch = (Q + P - 1) / P;
           const int64_t useful = Q * tpp;
           const int64_t slots = nch * rounds * ((T + 31) / 32) * 32;
-          consider(T, (int)P, 1, out_rows_total, useful, slots, P * in_plane, P * out_plane, 2 * P * wpp);
+          int64_t inb = P * in_plane;
+          if (pad_full)  // zero rows above each plane, below the last, and strip overrun
+            inb = P * npi * (zbe_b + round16(Hin * Win * eb)) + zbe_b + (int64_t)R * S * Win * eb;
+          p->padded = pad_full;
+          p->zbe = (int)(zbe_b / eb);
+          p->pitch = (int)((zbe_b + round16(Hin * Win * eb)) / eb);
+          consider(T, (int)P, 1, out_rows_total, useful, slots, inb, P * out_plane, 2 * P * wpp);
         }
       }
     }
@@ -229,6 +244,16 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
           const int64_t rounds = (tiles + T - 1) / T;
           const int64_t useful = tpp;
           const int64_t slots = (int64_t)nb * rounds * ((T + 31) / 32) * 32;
+          if (pad_band) {
+            const int64_t rows_buf = (fwd ? (int64_t)(br - 1) * S + K : (br + K - 1 + S - 1) / S + 1) + PADr;
+            inb = npi * (zbe_b + round16(rows_buf * Win * eb)) + zbe_b;
+          }
+          p->padded = pad_band;
+          p->zbe = (int)(zbe_b / eb);
+          if (pad_band) {
+            const int64_t rows_buf = (fwd ? (int64_t)(br - 1) * S + K : (br + K - 1 + S - 1) / S + 1) + PADr;
+            p->pitch = (int)((zbe_b + round16(rows_buf * Win * eb)) / eb);
+          }
           consider(T, 1, nb, br, useful, slots, inb, outb, 2 * wpp);
         }
       }
@@ -237,7 +262,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     *p = bestp;
     p->nchunks = (p->nbands == 1) ? (Q + p->P - 1) / p->P : Q * p->nbands;
     p->nsb = (p->band_rows + R - 1) / R;
-    KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi);
+    KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded);
     if (!fn) return false;
     const int occ = occupancy(fn, p->smem_bytes, p->threads);
     if (occ < 1) return false;
@@ -256,7 +281,21 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   const int nsb_full = (int)((g.Ho + R - 1) / R);
   double best = -1.0;
   ChunkPlan bestp = *p;
+  const int PADr = (K - 1) / 2;
+  const int64_t zbe_b = round16(PADr * g.W * eb);
+  const bool pad_full = (g.H * g.W * eb) % 16 == 0;
+  const bool pad_band = (g.W * eb) % 16 == 0;
   auto consider = [&](int P, int tpg, int nb, int br, int64_t xb, int64_t dyb) {
+    if (nb == 1 ? pad_full : pad_band) {  // padded x staging
+      const int64_t rows_buf = (nb == 1) ? g.H : (int64_t)(br - 1) * S + K + PADr;
+      const int64_t pitch_b = zbe_b + round16(rows_buf * g.W * eb);
+      xb = P * pitch_b + zbe_b + (int64_t)R * S * g.W * eb;
+      p->padded = true;
+      p->pitch = (int)(pitch_b / eb);
+      p->zbe = (int)(zbe_b / eb);
+    } else {
+      p->padded = false;
+    }
     const int T = P * m * tpg;
     if (T > kThreads || T < 64 || T % 32 != 0) return;  // whole warps: the reduction shuffles full warps
     ChunkPlan c = *p;
@@ -303,7 +342,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   *p = bestp;
   p->nsb = (p->band_rows + R - 1) / R;
   p->groups = (int)((g.C + p->P - 1) / p->P);
-  KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi);
+  KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded);
   if (!fn) return false;
   const int occ = occupancy(fn, p->smem_bytes, p->threads);
   if (occ < 1) return false;
@@ -332,6 +371,24 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   return nsl <= 128;
 }
 
+// Launch with programmatic dependent launch allowed (the kernels call
+// griddepcontrol.wait before touching global memory), so a kernel's launch and
+// prologue overlap the tail of the previous kernel on the stream.
+static cudaError_t launch(nchw::KernelFn fn, const ChunkPlan& p, cudaStream_t st, const nchw::NArgs& a) {
+  static const bool pdl = nchw::env_int("DWCONV_PDL", 1, 0, 1) == 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.grid);
+  cfg.blockDim = dim3((unsigned)p.threads);
+  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
 static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   nchw::NArgs a{};
   a.N = g.N; a.C = g.C; a.Q = g.N * g.C;
@@ -345,6 +402,7 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   a.in2_off = p.in2_off; a.in2_bytes = p.in2_bytes;
   a.out0_off = p.out0_off; a.out_stage = p.out_stage; a.out_bytes = p.out_bytes;
   a.ns = p.ns;
+  a.pitch = p.pitch; a.zbe = p.zbe;
   a.groups = p.groups; a.nslices = p.nslices; a.nps = p.n_per_slice; a.tpg = p.tpg;
   a.div_ncg = make_fastdiv((uint32_t)p.ncg);
   a.div_nsb = make_fastdiv((uint32_t)p.nsb);
@@ -357,18 +415,16 @@ cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, co
                             cudaStream_t st) {
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.w = w; a.out = y;
-  nchw::KernelFn fn = nchw::fwd_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi);
-  fn<<<p.grid, p.threads, p.smem_bytes, st>>>(a);
-  return cudaGetLastError();
+  nchw::KernelFn fn = nchw::fwd_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  return launch(fn, p, st, a);
 }
 
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,
                                  cudaStream_t st) {
   nchw::NArgs a = base_args(g, p);
   a.in = dy; a.w = w; a.out = dx;
-  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi);
-  fn<<<p.grid, p.threads, p.smem_bytes, st>>>(a);
-  return cudaGetLastError();
+  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  return launch(fn, p, st, a);
 }
 
 cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
@@ -378,9 +434,8 @@ cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void
   const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
   a.ws_ticket = static_cast<unsigned*>(ws);
   a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
-  nchw::KernelFn fn = nchw::bwd_filter_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi);
-  fn<<<p.grid, p.threads, p.smem_bytes, st>>>(a);
-  return cudaGetLastError();
+  nchw::KernelFn fn = nchw::bwd_filter_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  return launch(fn, p, st, a);
 }
 
 }  // namespace dwk

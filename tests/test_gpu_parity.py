@@ -206,3 +206,19 @@ def test_bad_descriptor_errors(_lib):
     with pytest.raises(_lib.DwconvError) as e:
         ops.dwconv_fwd(d, x, w, y)
     assert e.value.status == 3
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_mobilenet_layers_exact(dtype, _lib):
+    """Every MobileNet-v1 depthwise layer shape (Table III) at batch 2,
+    the exact launch configurations bench.py uses (planner picks per shape)."""
+    import synth
+    amax = 2 if dtype == "bf16" else 3
+    for L in synth.mobilenet_v1_dw(2):
+        check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=NCHW, dtype=dtype, kind="int", amax=amax)
+
+
+def test_mobilenet_layers_random_fp32(_lib):
+    import synth
+    for L in synth.mobilenet_v1_dw(2):
+        check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=NCHW, dtype="f32", kind="unif")
