@@ -354,6 +354,10 @@ def main():
         mean_ms = sum(durs) / len(durs)
         nbytes = pass_bytes(b["L"], pas, eb)
         kt.append(dict(layer=b["L"].name, pass_=pas, ms=mean_ms, bytes=nbytes, gbs=nbytes / (mean_ms * 1e-3) / 1e9))
+        if args.extra:
+            pl = ops.dwconv_plan(b["d"], {"fwd": 0, "bwd_data": 1, "bwd_filter": 2}[pas])
+            kt[-1]["plan"] = {k: pl[k] for k in ("variant_name", "grid", "block", "smem_bytes", "work_units",
+                                                 "planes_per_chunk", "rows_per_band", "batch_slices")}
     kernel_sum_ms = sum(k["ms"] for k in kt)
     dom = max(kt, key=lambda k: k["ms"])
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")

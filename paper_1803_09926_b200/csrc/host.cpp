@@ -180,7 +180,9 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
   Plan p;
   make_plan(g, DWCONV_PASS_FWD, di, &p);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
+  // the NCHW kernels store y with V-wide vector stores straight from registers
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(y) % 16) == 0)
+    return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
   return cuda_status(dwk::launch_generic_fwd(g, x, w, y, st));
 }
 
@@ -198,7 +200,8 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
   Plan p;
   make_plan(g, DWCONV_PASS_BWD_DATA, di, &p);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK)
+  // the NCHW kernels store dx with vector stores straight from registers
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0)
     return cuda_status(dwk::launch_nchw_bwd_data(g, p.chunk, dy, w, dx, st));
   return cuda_status(dwk::launch_generic_bwd_data(g, dy, w, dx, st));
 }

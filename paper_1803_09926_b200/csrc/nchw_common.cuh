@@ -99,6 +99,37 @@ __device__ __forceinline__ void prologue(unsigned char* smem, uint64_t* bars, co
   __syncthreads();
 }
 
+// Prologue of the warp-specialised kernels: "full" mbarriers at smem[0..64)
+// (count 1: the producer's arrive + TMA bytes), "empty" mbarriers at
+// smem[64..128) (count = consumer warps), zero row and input stages zeroed,
+// ordered before the TMA writes, then the programmatic-dependent-launch wait.
+__device__ __forceinline__ void prologue_ws(unsigned char* smem, const NArgs& a, int consumer_warps,
+                                            int full_count = 1) {
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 64);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.ns; ++i) {
+      mbar_init(&full[i], full_count);
+      mbar_init(&empty[i], consumer_warps);
+    }
+    fence_mbar_init();
+  }
+  auto zero = [&](uint32_t off, uint32_t bytes) {
+    uint4* p = reinterpret_cast<uint4*>(smem + off);
+    for (uint32_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+  };
+  zero(a.zrow_off - kZPad * 4, a.w_off - (a.zrow_off - kZPad * 4));
+  zero(a.in0_off, a.ns * a.in_stage);
+  fence_proxy_async_smem();
+  griddep_wait();
+  __syncthreads();
+}
+
+// Named barrier over the consumer warps only (warps 1..): barrier 1.
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
 // ------------------------------------------------------------------ vector I/O
 // N consecutive elements at p (aligned to min(16, N * sizeof(T)) bytes) <-> floats.
 template <class T, int N> struct VecIO;
@@ -247,6 +278,20 @@ __device__ __forceinline__ void stage_coop(T* base, const T* src0, const StageSp
 template <class T>
 __device__ __forceinline__ void zero_elems(T* p, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = T(0.f);
+}
+// Same over a subset of threads (thread t of nt).
+template <class T>
+__device__ __forceinline__ void zero_elems_n(T* p, int n, int t, int nt) {
+  for (int i = t; i < n; i += nt) p[i] = T(0.f);
+}
+template <class T>
+__device__ __forceinline__ void stage_coop_n(T* base, const T* src0, const StageSpec& s, int t, int nt) {
+  if (stage_contig<T>(s)) {
+    for (int64_t i = t; i < s.cnt * s.npl; i += nt) base[i] = src0[i];
+  } else {
+    for (int p = 0; p < s.npl; ++p)
+      for (int64_t i = t; i < s.cnt; i += nt) base[p * s.pitch + s.zbe + i] = src0[p * s.gstride + i];
+  }
 }
 
 // ------------------------------------------------------------------ stencil strip

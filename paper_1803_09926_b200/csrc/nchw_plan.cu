@@ -39,6 +39,11 @@ int num_stages() {
   return ns;
 }
 
+int num_stages_ws() {  // ring depth of the warp-specialised kernels
+  static int ns = env_int("DWCONV_WS_STAGES", 4, 2, 8);
+  return ns;
+}
+
 int occupancy(KernelFn fn, int smem, int threads) {
   static std::mutex mu;
   static KernelFn fns[512] = {};
@@ -118,19 +123,22 @@ namespace {
 int est_ctas_per_sm(int smem_bytes, int threads) {
   const int by_smem = (228 * 1024) / (smem_bytes + 1024);
   const int by_threads = 2048 / threads;
-  return std::max(0, std::min(std::min(by_smem, by_threads), 32));
+  const int by_regs = 65536 / (96 * threads);  // the kernels use ~60-110 registers per thread
+  return std::max(0, std::min(std::min(std::min(by_smem, by_threads), by_regs), 32));
 }
 
 // Score of a candidate chunking: fraction of issued thread-strip slots doing real
 // work, discounted when chunks are tiny (per-chunk fixed costs) or the SM holds
 // too few warps to hide shared-memory latency.
 double chunk_score(int64_t useful, int64_t slots, int64_t chunk_bytes, int smem, int threads) {
+  static const double min_chunk = 1024.0 * nchw::env_int("DWCONV_MIN_CHUNK_KB", 16, 1, 64);
+  static const double occ_warps = nchw::env_int("DWCONV_OCC_WARPS", 16, 4, 64);
   const double eff = (double)useful / (double)slots;
-  const double size_f = std::min(1.0, std::sqrt((double)chunk_bytes / (16.0 * 1024)));
+  const double size_f = std::min(1.0, std::sqrt((double)chunk_bytes / min_chunk));
   const int ctas = est_ctas_per_sm(smem, threads);
   if (ctas < 1) return -1.0;
   const double warps = (double)ctas * ((threads + 31) / 32);
-  const double occ_f = std::min(1.0, warps / 16.0);
+  const double occ_f = std::min(1.0, warps / occ_warps);
   return eff * size_f * occ_f;
 }
 
@@ -196,39 +204,48 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     };
     double best = -1.0;
     ChunkPlan bestp = *p;
-    auto consider = [&](int T, int P, int nbands, int band_rows, int64_t useful, int64_t slots, int64_t inb,
-                        int64_t outb, int64_t wb) {
+    const bool ws_design = true;  // warp-specialised: producer warp + direct stores
+    // Score a candidate: thread-strip slots used inside a chunk x chunks spread
+    // over the resident CTAs (tail) x pipeline fill (the first chunk of every CTA
+    // is exposed latency) x occupancy x a small-chunk penalty.
+    auto consider = [&](int T, int P, int nbands, int band_rows, int64_t tiles, int64_t nch, int64_t useful_total,
+                        int64_t inb, int64_t outb, int64_t wb) {
+      if (!ws_design && (int64_t)P * m * KK > 4 * T) return;  // bwd_data prefetches <= 4 weights per thread
       ChunkPlan c = *p;
-      c.threads = T; c.P = P; c.nbands = nbands; c.band_rows = band_rows;
+      if (ws_design) { outb = 0; c.in2_bytes = round128(wb / 2); wb = 0; }  // per-stage weight table
+      c.threads = T + (ws_design ? 32 : 0); c.P = P; c.nbands = nbands; c.band_rows = band_rows;
       c.in_bytes = round128(inb); c.out_bytes = round128(outb);
-      layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, ns);
+      const int nst = ws_design ? num_stages_ws() : ns;
+      layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, nst);
       if (c.smem_bytes > max_smem_optin) layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, 2);
       if (c.smem_bytes > max_smem_optin) return;
-      const double sc = chunk_score(useful, slots, inb + outb, c.smem_bytes, T);
+      const int ctas = est_ctas_per_sm(c.smem_bytes, c.threads);
+      if (ctas < 1) return;
+      const int64_t grid = std::min<int64_t>(nch, (int64_t)ctas * num_sms);
+      const int64_t rounds_c = (nch + grid - 1) / grid;
+      const int64_t rounds_t = (tiles + T - 1) / T;
+      const double eff = (double)useful_total / (double)(grid * rounds_c * rounds_t * ((T + 31) / 32) * 32);
+      const double pipe = (double)rounds_c / (rounds_c + 1.0);
+      const double warps = (double)std::min<int64_t>(ctas, (nch + num_sms - 1) / num_sms) * ((c.threads + 31) / 32);
+      const double occ_f = std::min(1.0, warps / 16.0);
+      const double size_f = std::min(1.0, std::sqrt((double)(inb + outb) / (4.0 * 1024)));
+      const double sc = eff * pipe * occ_f * size_f;
       if (sc > best) { best = sc; bestp = c; }
     };
     if (per <= budget_max) {  // whole-plane chunks
+      const int64_t pmax = std::min<int64_t>(Q, budget_max / per);
       for (int T : kT) {
-        for (int k = 1; k <= 4; ++k) {
-          int64_t P = (int64_t)k * T / tpp;
-          P = std::min<int64_t>(P, 4 * T / (m * KK));  // kernels prefetch <= 4 weights per thread
-          P = std::min<int64_t>(P, budget_max / per);
-          if (P >= al) P = P / al * al;
-          P = std::min<int64_t>(P, Q);
-          if (P < 1 || (P % al != 0 && P != Q)) continue;
+        for (int64_t P = al; P <= std::max<int64_t>(pmax, al); P += al) {
+          if (P > Q) break;
           const int64_t tiles = P * tpp;
-          const int64_t rounds = (tiles + T - 1) / T;
-          // work balance inside a chunk, and across the final partial chunk
           const int64_t nch = (Q + P - 1) / P;
-          const int64_t useful = Q * tpp;
-          const int64_t slots = nch * rounds * ((T + 31) / 32) * 32;
           int64_t inb = P * in_plane;
           if (pad_full)  // zero rows above each plane, below the last, and strip overrun
             inb = P * npi * (zbe_b + round16(Hin * Win * eb)) + zbe_b + (int64_t)R * S * Win * eb;
           p->padded = pad_full;
           p->zbe = (int)(zbe_b / eb);
           p->pitch = (int)((zbe_b + round16(Hin * Win * eb)) / eb);
-          consider(T, (int)P, 1, out_rows_total, useful, slots, inb, P * out_plane, 2 * P * wpp);
+          consider(T, (int)P, 1, out_rows_total, tiles, nch, Q * tpp, inb, P * out_plane, 2 * P * wpp);
         }
       }
     }
@@ -241,9 +258,6 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
         const int nb = (nsb_full + nsb_b - 1) / nsb_b;
         for (int T : kT) {
           const int64_t tiles = (int64_t)nsb_b * p->ncg;
-          const int64_t rounds = (tiles + T - 1) / T;
-          const int64_t useful = tpp;
-          const int64_t slots = (int64_t)nb * rounds * ((T + 31) / 32) * 32;
           if (pad_band) {
             const int64_t rows_buf = (fwd ? (int64_t)(br - 1) * S + K : (br + K - 1 + S - 1) / S + 1) + PADr;
             inb = npi * (zbe_b + round16(rows_buf * Win * eb)) + zbe_b;
@@ -254,7 +268,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
             const int64_t rows_buf = (fwd ? (int64_t)(br - 1) * S + K : (br + K - 1 + S - 1) / S + 1) + PADr;
             p->pitch = (int)((zbe_b + round16(rows_buf * Win * eb)) / eb);
           }
-          consider(T, 1, nb, br, useful, slots, inb, outb, 2 * wpp);
+          consider(T, 1, nb, br, tiles, Q * nb, Q * tpp, inb, outb, 2 * wpp);
         }
       }
     }
