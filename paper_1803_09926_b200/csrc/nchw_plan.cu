@@ -40,7 +40,7 @@ int num_stages() {
 }
 
 int num_stages_ws() {  // ring depth of the warp-specialised kernels
-  static int ns = env_int("DWCONV_WS_STAGES", 4, 2, 8);
+  static int ns = env_int("DWCONV_WS_STAGES", 3, 2, 8);
   return ns;
 }
 

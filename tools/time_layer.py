@@ -11,6 +11,7 @@ ap.add_argument("--passes", default="fwd,bwd_data,bwd_filter")
 ap.add_argument("--batches", default="16,64,256")
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--plan", action="store_true", help="append the chosen plan of the last batch")
 a = ap.parse_args()
 dt = torch.float32 if a.dtype == "f32" else torch.bfloat16
 eb = 4 if a.dtype == "f32" else 2
@@ -42,4 +43,9 @@ for lname in a.layers.split(","):
             us = times[len(times) // 2]
             nbytes = (L.x_elems() + L.y_elems()) * eb
             row.append((n, round(us, 2), round(nbytes / us / 1e3)))
-        print(lname, pas, row, flush=True)
+        extra = ""
+        if a.plan:
+            pi = ops.dwconv_plan(d, {"fwd": 0, "bwd_data": 1, "bwd_filter": 2}[pas])
+            extra = " ".join(f"{k}={pi[k]}" for k in ("variant_name", "grid", "block", "smem_bytes", "planes_per_chunk",
+                                                      "rows_per_band", "batch_slices"))
+        print(lname, pas, row, extra, flush=True)
