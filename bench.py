@@ -205,7 +205,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1803_09926_b200 as dwl
-    from paper_1803_09926_b200 import ops
+    from paper_1803_09926_b200 import dp, ops
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -229,19 +229,17 @@ def main():
         t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=gen)
         return t.to(dtype).contiguous(memory_format=mf) if len(shape) == 4 else t.to(dtype)
 
-    wcount = sum(L.w_elems() for L in layers)
-    dw_bucket = torch.zeros(wcount, dtype=torch.float32, device=dev)
+    bucket = dp.DwBucket([(L.c * L.m, L.k, L.k) for L in layers], device=dev)  # every layer's dw, one all-reduce
+    dw_bucket = bucket.flat
     bufs = []
-    off = 0
     for L in layers:
         d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout, dcode)
         b = dict(L=L, d=d, x=rnd((L.n, L.c, L.h, L.w)), w=rnd((L.c * L.m, L.k, L.k)),
                  dy=rnd((L.n, L.c * L.m, L.ho, L.wo)),
                  y=torch.empty((L.n, L.c * L.m, L.ho, L.wo), dtype=tdt, device=dev, memory_format=mf),
                  dx=torch.empty((L.n, L.c, L.h, L.w), dtype=tdt, device=dev, memory_format=mf),
-                 dw=dw_bucket[off:off + L.w_elems()].view(L.c * L.m, L.k, L.k),
+                 dw=bucket.views[len(bufs)],
                  wsb=ops.dwconv_bwd_filter_workspace_bytes(d))
-        off += L.w_elems()
         bufs.append(b)
     ws = torch.zeros(max(16, max(b["wsb"] for b in bufs)), dtype=torch.uint8, device=dev)
     footprint = sum(b[k].numel() * b[k].element_size() for b in bufs for k in ("x", "w", "dy", "y", "dx"))
@@ -303,7 +301,7 @@ def main():
         else:
             step_kernels()
         if world > 1:
-            dist.all_reduce(dw_bucket)
+            bucket.allreduce()
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -401,7 +399,7 @@ def main():
                 b["w"].copy_(hw, non_blocking=True)
             step_kernels()
             if world > 1:
-                dist.all_reduce(dw_bucket)
+                bucket.allreduce()
             host_dw.copy_(dw_bucket, non_blocking=True)
 
         with torch.cuda.stream(stream):
