@@ -4,7 +4,7 @@
 // over exact divisions in range -- the adjoint of the forward pass (DESIGN.md
 // reading R9; the paper delegates it to the framework).
 //  * S = 1: the forward stencil on dy with the kernel flipped (weights are staged
-//    flipped), strip = R dx rows x V dx columns, packed FFMA2.
+//    flipped on read), strip = R dx rows x V dx columns, packed FFMA2.
 //  * S = 2: polyphase tile of R dx rows x S dx columns aligned to the stride so
 //    the tap -> dy mapping is static.
 // Per-j partial sums keep each serial chain at K*K (R5 iii).  Same warp-
@@ -25,7 +25,7 @@ __device__ __forceinline__ ChunkRows bd_rows(const NArgs& a, int64_t c) {
     k.np = (int)min((int64_t)a.P, a.Q - k.q0);
     k.r0 = 0; k.r1 = a.H; k.lo = 0; k.hi = a.Ho;
   } else {
-    k.q0 = c / a.nbands;
+    k.q0 = (int64_t)fdiv((uint32_t)c, a.div_nb);
     const int b = (int)(c - k.q0 * a.nbands);
     k.np = 1;
     k.r0 = b * a.BR;
@@ -79,26 +79,32 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
     for (int64_t c = blockIdx.x; c < a.nchunks; c += gridDim.x, ++it) {
       if (it >= a.ns) mbar_wait(&empty[s], ph ^ 1);  // consumers released the stage
       const ChunkRows k = bd_rows<K, S>(a, c);
+      const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
       if (threadIdx.x == 0) {
         const StageSpec sp = spec_of(k);
-        if (stage_bulk_ok<T>(src_of(k), sp)) {
-          mbar_arrive_expect_tx(&full[s], stage_bytes<T>(sp));
-          stage_copy<T>(sin_of(s), src_of(k), sp, &full[s]);
+        const bool xb = stage_bulk_ok<T>(src_of(k), sp);  // else consumers copy this chunk themselves
+        const uint32_t tx = (xb ? stage_bytes<T>(sp) : 0u) + (ww.tma ? ww.bytes : 0u);
+        if (tx) {
+          mbar_arrive_expect_tx(&full[s], tx);
+          if (xb) stage_copy<T>(sin_of(s), src_of(k), sp, &full[s]);
+          if (ww.tma) bulk_g2s(sw_of(s), wt + ww.a0, ww.bytes, &full[s]);
         } else {
-          mbar_arrive(&full[s]);  // consumers copy this chunk themselves
+          mbar_arrive(&full[s]);
         }
       }
-      // the producer warp stages the chunk's weights (fp32; flipped for S == 1)
-      const int cbase = (int)(k.q0 % a.C) * m;
-      float* sw = sw_of(s);
-      for (int idx = threadIdx.x; idx < k.np * m * KK; idx += 32) {
-        const int pl = idx / KK, q = idx - pl * KK;
-        const uint32_t ov = (uint32_t)(cbase + pl);
-        const int o = (int)(ov - fdiv(ov, a.div_co) * (uint32_t)a.Co);
-        sw[idx] = Elem<T>::ldg(wt + (int64_t)o * KK + ((S == 1) ? (KK - 1 - q) : q));
+      if (!ww.tma) {  // fallback: the producer warp writes the weights as an fp32 table (flipped for S == 1)
+        __syncwarp();
+        const int cbase = (int)(k.q0 % a.C) * m;
+        float* sw = sw_of(s);
+        for (int idx = threadIdx.x; idx < k.np * m * KK; idx += 32) {
+          const int pl = idx / KK, q = idx - pl * KK;
+          const uint32_t ov = (uint32_t)(cbase + pl);
+          const int o = (int)(ov - fdiv(ov, a.div_co) * (uint32_t)a.Co);
+          sw[idx] = Elem<T>::ldg(wt + (int64_t)o * KK + ((S == 1) ? (KK - 1 - q) : q));
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      if (threadIdx.x == 0) mbar_arrive(&full[s]);  // second arrival: weights are in smem
+      if (threadIdx.x == 0) mbar_arrive(&full[s]);  // second arrival: the weight table is written
       if (++s == a.ns) { s = 0; ph ^= 1; }
     }
   } else {
@@ -121,6 +127,8 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
         consumer_sync(nct);
       }
       const float* swc = sw_of(s);
+      const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
+      const T* swr = reinterpret_cast<const T*>(swc) + ww.off;  // raw rows (ww.tma), flipped on read for S == 1
       const int rows_dy = k.hi - k.lo;
       const int ntiles = k.np * a.nsb * ncg;
       for (int t = ctid; t < ntiles; t += nct) {
@@ -136,10 +144,16 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
 #pragma unroll
           for (int u = 0; u < TW; ++u) acc[tt][u] = 0.f;
         for (int j = 0; j < m; ++j) {
-          const float* wp = swc + (pp * m + j) * KK;
           float wr[KK];
+          if (ww.tma) {
+            const T* wp = swr + (pp * m + j) * KK;
 #pragma unroll
-          for (int q = 0; q < KK; ++q) wr[q] = wp[q];
+            for (int q = 0; q < KK; ++q) wr[q] = Elem<T>::load(wp + ((S == 1) ? (KK - 1 - q) : q));
+          } else {
+            const float* wp = swc + (pp * m + j) * KK;
+#pragma unroll
+            for (int q = 0; q < KK; ++q) wr[q] = wp[q];
+          }
           float part[R][TW];
 #pragma unroll
           for (int tt = 0; tt < R; ++tt)

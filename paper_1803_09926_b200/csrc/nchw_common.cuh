@@ -44,6 +44,9 @@ struct NArgs {
   int ns;
   int groups, nslices, nps, tpg;
   FastDiv div_ncg, div_nsb, div_m, div_co;
+  FastDiv div_c, div_nb;  // channel of a plane index; chunk -> (plane, band)
+  int wbulk;              // w is 16-B aligned with a 16-B multiple size: weight rows may be bulk-copied
+  int dbg;                // tuning aid (DWCONV_DEBUG): 1 = skip compute, 2 = skip stores
 };
 
 using KernelFn = void (*)(NArgs);
@@ -292,6 +295,32 @@ __device__ __forceinline__ void stage_coop_n(T* base, const T* src0, const Stage
     for (int p = 0; p < s.npl; ++p)
       for (int64_t i = t; i < s.cnt; i += nt) base[p * s.pitch + s.zbe + i] = src0[p * s.gstride + i];
   }
+}
+
+// ------------------------------------------------------------------ chunk weights
+// A chunk of planes [q0, q0+np) (plane q = n*C + c) needs the weight rows of the
+// output channels [cb*m, (cb+np)*m), cb = q0 mod C: elements [e0, e1) of w.
+// When that range does not wrap past channel C-1 and a.wbulk holds, the producer
+// stages the 16-B aligned superset [a0, a1) raw (storage dtype) with one bulk
+// copy on the stage's full barrier, and consumers read element e at
+// table + off + (e - e0).  Otherwise the producer warp writes an fp32 table.
+struct WeightWin {
+  bool tma;
+  int off;        // elements from the staged start a0 to e0
+  int64_t a0;     // first staged element
+  uint32_t bytes; // staged bytes
+};
+template <class T, int KK>
+__device__ __forceinline__ WeightWin weight_win(const NArgs& a, int64_t q0, int np) {
+  constexpr int64_t A = 16 / sizeof(T);
+  WeightWin r;
+  const int64_t cb = q0 - (int64_t)fdiv((uint32_t)q0, a.div_c) * a.C;
+  r.tma = a.wbulk && cb + np <= a.C;
+  const int64_t e0 = cb * a.m * KK, e1 = (cb + np) * a.m * KK;
+  r.a0 = e0 & ~(A - 1);
+  r.bytes = (uint32_t)((((e1 + A - 1) & ~(A - 1)) - r.a0) * (int64_t)sizeof(T));
+  r.off = (int)(e0 - r.a0);
+  return r;
 }
 
 // ------------------------------------------------------------------ stencil strip

@@ -28,7 +28,7 @@ __device__ __forceinline__ ChunkRows fwd_rows(const NArgs& a, int64_t c) {
     k.np = (int)min((int64_t)a.P, a.Q - k.q0);
     k.r0 = 0; k.r1 = a.Ho; k.lo = 0; k.hi = a.H;
   } else {
-    k.q0 = c / a.nbands;
+    k.q0 = (int64_t)fdiv((uint32_t)c, a.div_nb);
     const int b = (int)(c - k.q0 * a.nbands);
     k.np = 1;
     k.r0 = b * a.BR;
@@ -72,21 +72,23 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
     int it = 0;
     for (int64_t c = blockIdx.x; c < a.nchunks; c += gridDim.x, ++it) {
       if (it >= a.ns) mbar_wait(&empty[s], ph ^ 1);  // consumers released the stage
+      const ChunkRows k = fwd_rows<K, S>(a, c);
+      const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
       if (threadIdx.x == 0) {
-        const ChunkRows k = fwd_rows<K, S>(a, c);
         const T* src = x + (k.q0 * a.H + k.lo) * W;
         const StageSpec sp = spec_of(k);
-        if (stage_bulk_ok<T>(src, sp)) {
-          mbar_arrive_expect_tx(&full[s], stage_bytes<T>(sp));
-          stage_copy<T>(sin_of(s), src, sp, &full[s]);
+        const bool xb = stage_bulk_ok<T>(src, sp);  // else consumers copy this chunk themselves
+        const uint32_t tx = (xb ? stage_bytes<T>(sp) : 0u) + (ww.tma ? ww.bytes : 0u);
+        if (tx) {
+          mbar_arrive_expect_tx(&full[s], tx);
+          if (xb) stage_copy<T>(sin_of(s), src, sp, &full[s]);
+          if (ww.tma) bulk_g2s(sw_of(s), wt + ww.a0, ww.bytes, &full[s]);
         } else {
-          mbar_arrive(&full[s]);  // consumers copy this chunk themselves
+          mbar_arrive(&full[s]);
         }
       }
-      __syncwarp();
-      // the whole producer warp stages the chunk's weights (fp32) next to its input
-      {
-        const ChunkRows k = fwd_rows<K, S>(a, c);
+      if (!ww.tma) {  // fallback: the producer warp writes the chunk's weights as an fp32 table
+        __syncwarp();
         const int cbase = (int)(k.q0 % a.C) * m;
         float* sw = sw_of(s);
         for (int idx = threadIdx.x; idx < k.np * m * KK; idx += 32) {
@@ -95,9 +97,9 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
           const int o = (int)(ov - fdiv(ov, a.div_co) * (uint32_t)a.Co);
           sw[idx] = Elem<T>::ldg(wt + (int64_t)o * KK + q);
         }
+        __syncwarp();
       }
-      __syncwarp();
-      if (threadIdx.x == 0) mbar_arrive(&full[s]);  // second arrival: weights are in smem
+      if (threadIdx.x == 0) mbar_arrive(&full[s]);  // second arrival: the weight table is written
       if (++s == a.ns) { s = 0; ph ^= 1; }
     }
   } else {
@@ -122,7 +124,9 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
       const int rows_in = k.hi - k.lo;
       const int npl = k.np * m;
       const float* swc = sw_of(s);
-      const int ntiles = npl * a.nsb * ncg;
+      const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
+      const T* swr = reinterpret_cast<const T*>(swc) + ww.off;  // raw rows (ww.tma)
+      const int ntiles = (a.dbg & 1) ? 0 : npl * a.nsb * ncg;
       for (int t = ctid; t < ntiles; t += nct) {
         const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
         const int c0 = (t - t2 * ncg) * V;
@@ -131,8 +135,13 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
         const int pin = (int)fdiv((uint32_t)pp, a.div_m);
         const int oh0 = k.r0 + sb * R;
         float wr[KK];
+        if (ww.tma) {
 #pragma unroll
-        for (int q = 0; q < KK; ++q) wr[q] = swc[pp * KK + q];
+          for (int q = 0; q < KK; ++q) wr[q] = Elem<T>::load(swr + pp * KK + q);
+        } else {
+#pragma unroll
+          for (int q = 0; q < KK; ++q) wr[q] = swc[pp * KK + q];
+        }
         float acc[R][V];
 #pragma unroll
         for (int tt = 0; tt < R; ++tt)
@@ -143,7 +152,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
         T* yo = y + ((k.q0 * m + pp) * a.Ho + oh0) * Wo + c0;
 #pragma unroll
         for (int tt = 0; tt < R; ++tt)
-          if (oh0 + tt < k.r1) VecIO<T, V>::store(yo + tt * Wo, acc[tt]);
+          if (oh0 + tt < k.r1 && !(a.dbg & 2)) VecIO<T, V>::store(yo + tt * Wo, acc[tt]);
       }
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);

@@ -154,7 +154,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   if (g.ph != (K - 1) / 2 || g.pw != (K - 1) / 2) return false;
   if (g.m < 1 || g.m > 8) return false;
   if (g.H > 8192 || g.W > 8192 || g.Ho * g.Wo * (int64_t)g.m > (1 << 24)) return false;
-  if (g.N * g.C > (int64_t)1 << 40) return false;
+  if (g.N * g.C >= (int64_t)1 << 31) return false;  // plane and chunk indices use 32-bit magic division
   // strided windows must stay inside the row (odd W with S = 2 goes to the generic path)
   if (pass != DWCONV_PASS_BWD_DATA && S * g.Wo > g.W) return false;
   *p = ChunkPlan{};
@@ -212,7 +212,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
                         int64_t inb, int64_t outb, int64_t wb) {
       if (!ws_design && (int64_t)P * m * KK > 4 * T) return;  // bwd_data prefetches <= 4 weights per thread
       ChunkPlan c = *p;
-      if (ws_design) { outb = 0; c.in2_bytes = round128(wb / 2); wb = 0; }  // per-stage weight table
+      if (ws_design) { outb = 0; c.in2_bytes = round128(wb / 2 + 32); wb = 0; }  // per-stage weight table (+ bulk-copy alignment slack)
       c.threads = T + (ws_design ? 32 : 0); c.P = P; c.nbands = nbands; c.band_rows = band_rows;
       c.in_bytes = round128(inb); c.out_bytes = round128(outb);
       const int nst = ws_design ? num_stages_ws() : ns;
@@ -275,6 +275,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     if (best < 0.0) return false;
     *p = bestp;
     p->nchunks = (p->nbands == 1) ? (Q + p->P - 1) / p->P : Q * p->nbands;
+    if (p->nchunks >= ((int64_t)1 << 31)) return false;
     p->nsb = (p->band_rows + R - 1) / R;
     KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded);
     if (!fn) return false;
@@ -403,6 +404,13 @@ static cudaError_t launch(nchw::KernelFn fn, const ChunkPlan& p, cudaStream_t st
   return cudaLaunchKernelEx(&cfg, fn, a);
 }
 
+// Weight rows may be staged by bulk copy (16-B aligned base and total size).
+static int weights_bulk_ok(const Geom& g, const void* w) {
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  const int64_t bytes = g.C * g.m * g.kh * g.kw * eb;
+  return ((reinterpret_cast<uintptr_t>(w) & 15u) == 0 && bytes % 16 == 0) ? 1 : 0;
+}
+
 static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   nchw::NArgs a{};
   a.N = g.N; a.C = g.C; a.Q = g.N * g.C;
@@ -422,6 +430,10 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   a.div_nsb = make_fastdiv((uint32_t)p.nsb);
   a.div_m = make_fastdiv((uint32_t)g.m);
   a.div_co = make_fastdiv((uint32_t)a.Co);
+  a.div_c = make_fastdiv((uint32_t)g.C);
+  static const int dbg = nchw::env_int("DWCONV_DEBUG", 0, 0, 3);
+  a.dbg = dbg;
+  a.div_nb = make_fastdiv((uint32_t)std::max(1, p.nbands));
   return a;
 }
 
@@ -429,6 +441,7 @@ cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, co
                             cudaStream_t st) {
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.w = w; a.out = y;
+  a.wbulk = weights_bulk_ok(g, w);
   nchw::KernelFn fn = nchw::fwd_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
   return launch(fn, p, st, a);
 }
@@ -437,6 +450,7 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
                                  cudaStream_t st) {
   nchw::NArgs a = base_args(g, p);
   a.in = dy; a.w = w; a.out = dx;
+  a.wbulk = weights_bulk_ok(g, w);
   nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
   return launch(fn, p, st, a);
 }

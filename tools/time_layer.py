@@ -12,10 +12,12 @@ ap.add_argument("--batches", default="16,64,256")
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--plan", action="store_true", help="append the chosen plan of the last batch")
+ap.add_argument("--flush-mb", type=int, default=256, help="bytes read between reps to evict L2 (keeps the GPU busy while the host enqueues)")
+ap.add_argument("--graph", action="store_true", help="replay the launch from a CUDA graph (no host launch overhead)")
 a = ap.parse_args()
 dt = torch.float32 if a.dtype == "f32" else torch.bfloat16
 eb = 4 if a.dtype == "f32" else 2
-flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB, read to evict L2 cleanly
+flush = torch.ones(a.flush_mb << 18, dtype=torch.float32, device="cuda")  # 256 MB, read to evict L2 cleanly
 sink = torch.empty(1, device="cuda")
 for lname in a.layers.split(","):
     for pas in a.passes.split(","):
@@ -32,6 +34,12 @@ for lname in a.layers.split(","):
             f = {"fwd": lambda: ops.dwconv_fwd(d, x, w, y), "bwd_data": lambda: ops.dwconv_bwd_data(d, dy, w, dx),
                  "bwd_filter": lambda: ops.dwconv_bwd_filter(d, x, dy, dw, ws)}[pas]
             for _ in range(3): f()
+            if a.graph:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    f()
+                f = g.replay
             times = []
             for _ in range(a.reps):
                 torch.sum(flush, dim=0, keepdim=True, out=sink)
