@@ -231,7 +231,10 @@ int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float
   if (g.N == 0) return cuda_status(cudaMemsetAsync(dw, 0, (size_t)(g.C * g.m * g.kh * g.kw) * 4, st));
   Plan p;
   make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) {
+  // the register-direct variant needs 16-B aligned x and dy (vector loads)
+  const bool direct_ok =
+      !p.chunk.direct || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0;
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && direct_ok) {
     if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
     if (!workspace) return DWCONV_ERR_NULL_POINTER;
     if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;

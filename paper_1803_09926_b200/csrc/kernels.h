@@ -52,6 +52,9 @@ struct ChunkPlan {
   int tpg;              // threads per dy plane
   int max_chain;        // worst-case serial depth of the dw sums
   size_t ws_bytes;      // workspace
+  // bwd_filter register-direct variant (direct_bwd_filter.cu): no smem staging
+  bool direct;
+  int dL, dSPW, dspc;   // lanes per row set, row sets per warp, row sets per channel
 };
 
 // Returns false if the NCHW chunk family cannot handle the geometry.

@@ -234,6 +234,13 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
   griddep_launch_dependents();
 }
 
+// V = 8 (one 16-B row load per window) exists for bf16 3x3 only.
+template <class T, int K, int S, int R, bool PD>
+KernelFn v8_kernel() {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value && K == 3 && PD) return nchw_bwd_data_kernel<T, K, S, R, 8, PD>;
+  else return nullptr;
+}
+
 template <class T, int K, int S, bool PD>
 KernelFn pick_rv(int RI, int VI) {
   constexpr int R0 = rows_bd(K, S, 0), R1 = rows_bd(K, S, 1);
@@ -243,6 +250,7 @@ KernelFn pick_rv(int RI, int VI) {
     case 0: return nchw_bwd_data_kernel<T, K, S, R, 1, PD>;       \
     case 1: return nchw_bwd_data_kernel<T, K, S, R, 2, PD>;       \
     case 2: return PD ? nchw_bwd_data_kernel<T, K, S, R, 4, PD> : nullptr; \
+    case 3: return v8_kernel<T, K, S, R, PD>();                 \
     default: return nullptr;                                      \
   }
     if (RI == 0) { DW_V(R0) } else { DW_V(R1) }

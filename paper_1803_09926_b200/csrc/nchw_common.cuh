@@ -14,6 +14,8 @@
 
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -379,4 +381,23 @@ __device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, i
 }
 
 }  // namespace nchw
+
+namespace direct {
+// Arguments of the register-direct bwd_filter kernels (direct_bwd_filter.cu).
+struct DArgs {
+  const void* x;
+  const void* dy;
+  float* dw;
+  float* ws_part;       // per-slice partials [nslices][Co][9]
+  unsigned* ws_ticket;  // [groups]
+  int N, C, m, Co, H, W, Ho, Wo;
+  int P;                // output channels per group
+  int groups, nslices, nps;
+  int L, SPW, spc;      // lanes per row set, row sets per warp, row sets per channel
+  int nsb;              // dy strips per plane
+  int pf;               // rows are 16-B multiples and bases aligned: bulk L2 prefetch allowed
+};
+using DKernelFn = void (*)(DArgs);
+DKernelFn bwd_filter_kernel(int dtype, int S, int R, int V);
+}  // namespace direct
 }  // namespace dwk

@@ -7,6 +7,7 @@
 // GPU while keeping every dw serial chain short (dwconv_plan reports max_chain).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -72,10 +73,11 @@ int ilog2_ceil(int64_t v) {
   return l;
 }
 
-// Column-vector variant: V = 4, 2 or 1 output columns per thread.  Needs the
+// Column-vector variant: V = 8 (bf16 3x3), 4, 2 or 1 output columns per thread.  Needs the
 // output width divisible by V and the input rows aligned for the S*V vector load.
-int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb) {
-  for (int vi = 2; vi > 0; --vi) {
+int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb, int K) {
+  static const int v8 = env_int("DWCONV_BF16_V8", 1, 0, 1);
+  for (int vi = (eb == 2 && K == 3 && v8) ? 3 : 2; vi > 0; --vi) {
     const int64_t V = 1 << vi;
     const int64_t align = std::min<int64_t>(16, S * V * eb);
     if (out_w % V == 0 && (in_w * eb) % align == 0 && (out_w * eb) % std::min<int64_t>(16, V * eb) == 0) return vi;
@@ -144,6 +146,58 @@ double chunk_score(int64_t useful, int64_t slots, int64_t chunk_bytes, int smem,
 
 }  // namespace
 
+// Register-direct bwd_filter (direct_bwd_filter.cu) for K = 3, pad 1: a row set
+// of L = Wo / V lanes covers an output row, so Wo / V <= 32; rows must be
+// aligned for the vector loads.  Work: P = row sets per warp output channels per
+// CTA (8 row sets each), ~DWCONV_DBF_TASKS tasks (image x strip) per row set.
+static bool plan_direct_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p) {
+  static const bool on = nchw::env_int("DWCONV_DIRECT_BF", 1, 0, 1) == 1;
+  static const int tasks = nchw::env_int("DWCONV_DBF_TASKS", 4, 1, 64);
+  static const int max_wo = nchw::env_int("DWCONV_DBF_MAXWO", 8, 1, 4096);
+  if (!on || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1 || g.Wo > max_wo) return false;
+  const int S = g.sh;
+  if (g.sw != S || (S != 1 && S != 2) || g.W != S * g.Wo) return false;
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  int V = 0;
+  for (int v : {8, 4, 2, 1}) {
+    if (v * eb > 16 || g.Wo % v != 0 || g.Wo / v > 32) continue;
+    if (S == 2 && v * eb > 8) continue;  // 2*V columns of x per lane: keep the window in registers
+    const int64_t nx = std::min<int64_t>(16, (int64_t)S * v * eb);
+    if ((g.W * eb) % nx != 0 || (g.Wo * eb) % std::min<int64_t>(16, v * eb) != 0) continue;
+    V = v;
+    break;
+  }
+  if (V == 0) return false;
+  const int R = (g.Ho % 7 == 0) ? 7 : 8;
+  if (!direct::bwd_filter_kernel(g.dtype, S, R, V)) return false;
+  const int L = (int)(g.Wo / V), SPW = 32 / L, P = SPW, spc = 8;
+  const int Co = (int)(g.C * g.m);
+  const int nsb = (int)((g.Ho + R - 1) / R);
+  const int64_t N = std::max<int64_t>(g.N, 1);
+  const int64_t groups = (Co + P - 1) / P;
+  int64_t nps = std::min<int64_t>(N, std::max<int64_t>(1, ((int64_t)tasks * spc + nsb - 1) / nsb));
+  nps = std::max<int64_t>(nps, (N + 127) / 128);
+  while (nps > 1 && groups * ((N + nps - 1) / nps) < 2 * num_sms && (nps + 1) / 2 >= (N + 127) / 128) nps = (nps + 1) / 2;
+  const int64_t nsl = (N + nps - 1) / nps;
+  *p = ChunkPlan{};
+  p->direct = true;
+  p->threads = 256;
+  p->smem_bytes = 0;
+  p->R = R; p->V = V; p->ri = (R == 7) ? 0 : 1;
+  p->P = P; p->nbands = 1; p->band_rows = (int)g.Ho; p->nsb = nsb; p->ncg = L;
+  p->dL = L; p->dSPW = SPW; p->dspc = spc;
+  p->groups = (int)groups; p->nslices = (int)nsl; p->n_per_slice = (int)nps; p->tpg = L;
+  p->grid = (int)(groups * nsl);
+  p->nchunks = p->grid;
+  const bool packed = (S == 1 && V % 2 == 0);
+  const int64_t per_task = (int64_t)R * (packed ? V / 2 : V) + (packed ? 1 : 0);
+  const int64_t task_sum = (nps * nsb + spc - 1) / spc;
+  p->max_chain = (int)(per_task + task_sum + L + spc + 2 * nchw::ilog2_ceil(nsl) + 1);
+  const size_t tick = ((size_t)groups * 4 + 15) / 16 * 16;
+  p->ws_bytes = tick + (size_t)nsl * Co * 9 * 4;
+  return p->max_chain <= 160 && groups * nsl < (int64_t)1 << 31;
+}
+
 bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* p) {
   using namespace nchw;
   if (g.layout != DWCONV_NCHW) return false;
@@ -185,8 +239,8 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     const int out_rows_total = fwd ? (int)g.Ho : (int)g.H;
     p->ri = (out_rows_total % rows_for(pass, K, S, 0) == 0) ? 0 : 1;
     p->R = rows_for(pass, K, S, p->ri);
-    if (fwd) p->vi = pick_vi(g.Wo, g.W, S, eb);
-    else p->vi = (S == 1) ? pick_vi(g.W, g.Wo, 1, eb) : 0;
+    if (fwd) p->vi = pick_vi(g.Wo, g.W, S, eb, K);
+    else p->vi = (S == 1) ? pick_vi(g.W, g.Wo, 1, eb, K) : 0;
     p->V = 1 << p->vi;
     p->ncg = fwd ? (int)(g.Wo / p->V) : (S == 1 ? (int)(g.W / p->V) : (int)((g.W + S - 1) / S));
     const int R = p->R;
@@ -211,6 +265,14 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     auto consider = [&](int T, int P, int nbands, int band_rows, int64_t tiles, int64_t nch, int64_t useful_total,
                         int64_t inb, int64_t outb, int64_t wb) {
       if (!ws_design && (int64_t)P * m * KK > 4 * T) return;  // bwd_data prefetches <= 4 weights per thread
+      // tuning aid: DWCONV_FD_FORCE="T,P,band_rows" (band_rows 0 = whole planes) pins the chunk shape
+      static const int* force = []() -> const int* {
+        static int f[3];
+        const char* e = getenv("DWCONV_FD_FORCE");
+        if (!e || sscanf(e, "%d,%d,%d", &f[0], &f[1], &f[2]) != 3) return nullptr;
+        return f;
+      }();
+      if (force && (T != force[0] || P != force[1] || (nbands == 1 ? 0 : band_rows) != force[2])) return;
       ChunkPlan c = *p;
       if (ws_design) { outb = 0; c.in2_bytes = round128(wb / 2 + 32); wb = 0; }  // per-stage weight table (+ bulk-copy alignment slack)
       c.threads = T + (ws_design ? 32 : 0); c.P = P; c.nbands = nbands; c.band_rows = band_rows;
@@ -219,17 +281,22 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, nst);
       if (c.smem_bytes > max_smem_optin) layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, 2);
       if (c.smem_bytes > max_smem_optin) return;
-      const int ctas = est_ctas_per_sm(c.smem_bytes, c.threads);
+      KernelFn kf = kernel_for(pass, g.dtype, K, S, c.ri, c.vi, c.padded);
+      const int ctas = kf ? occupancy(kf, c.smem_bytes, c.threads) : 0;  // resident CTAs per SM
       if (ctas < 1) return;
       const int64_t grid = std::min<int64_t>(nch, (int64_t)ctas * num_sms);
       const int64_t rounds_c = (nch + grid - 1) / grid;
       const int64_t rounds_t = (tiles + T - 1) / T;
       const double eff = (double)useful_total / (double)(grid * rounds_c * rounds_t * ((T + 31) / 32) * 32);
       const double pipe = (double)rounds_c / (rounds_c + 1.0);
-      const double warps = (double)std::min<int64_t>(ctas, (nch + num_sms - 1) / num_sms) * ((c.threads + 31) / 32);
+      const double ctas_eff = (double)std::min<int64_t>(ctas, (nch + num_sms - 1) / num_sms);
+      const double warps = ctas_eff * ((c.threads + 31) / 32);
       const double occ_f = std::min(1.0, warps / 16.0);
       const double size_f = std::min(1.0, std::sqrt((double)(inb + outb) / (4.0 * 1024)));
-      const double sc = eff * pipe * occ_f * size_f;
+      // bytes in flight per SM: every resident CTA keeps its ring of input stages loading
+      static const double fill_b = 1024.0 * env_int("DWCONV_FILL_KB", 160, 8, 228);
+      const double fill_f = std::min(1.0, ctas_eff * c.ns * (double)c.in_bytes / fill_b);
+      const double sc = eff * pipe * occ_f * size_f * fill_f;
       if (sc > best) { best = sc; bestp = c; }
     };
     if (per <= budget_max) {  // whole-plane chunks
@@ -286,10 +353,11 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   }
 
   // ---------------- bwd_filter
+  if (plan_direct_bwd_filter(g, num_sms, p)) return true;
   const int64_t per = x_plane + y_plane;
   p->ri = (g.Ho % rows_bf(K, 0) == 0) ? 0 : 1;
   p->R = rows_bf(K, p->ri);
-  p->vi = pick_vi(g.Wo, g.W, S, eb);
+  p->vi = pick_vi(g.Wo, g.W, S, eb, K);
   p->V = 1 << p->vi;
   p->ncg = (int)(g.Wo / p->V);
   const int R = p->R;
@@ -457,6 +525,34 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
 
 cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
                                    void* ws, cudaStream_t st) {
+  const size_t tk = ((size_t)p.groups * 4 + 15) / 16 * 16;
+  if (p.direct) {
+    direct::DArgs d{};
+    d.x = x; d.dy = dy; d.dw = dw;
+    d.ws_ticket = static_cast<unsigned*>(ws);
+    d.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tk);
+    d.N = (int)g.N; d.C = (int)g.C; d.m = g.m; d.Co = (int)(g.C * g.m);
+    d.H = (int)g.H; d.W = (int)g.W; d.Ho = (int)g.Ho; d.Wo = (int)g.Wo;
+    d.P = p.P; d.groups = p.groups; d.nslices = p.nslices; d.nps = p.n_per_slice;
+    d.L = p.dL; d.SPW = p.dSPW; d.spc = p.dspc; d.nsb = p.nsb;
+    static const int pf_env = nchw::env_int("DWCONV_DBF_PF", 1, 0, 1);
+    const int64_t ebb = (g.dtype == DWCONV_F32) ? 4 : 2;
+    d.pf = pf_env && (g.W * ebb) % 16 == 0 && (g.Wo * ebb) % 16 == 0 &&
+           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
+    direct::DKernelFn fn = direct::bwd_filter_kernel(g.dtype, g.sh, p.R, p.V);
+    static const bool pdl = nchw::env_int("DWCONV_PDL", 1, 0, 1) == 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.grid);
+    cfg.blockDim = dim3((unsigned)p.threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, d);
+  }
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.in2 = dy; a.dw = dw;
   const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
