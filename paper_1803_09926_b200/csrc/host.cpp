@@ -16,6 +16,7 @@ namespace {
 
 using dwk::ChunkPlan;
 using dwk::Geom;
+using dwk::NhwcPlan;
 
 std::atomic<int> g_override{0};
 
@@ -94,6 +95,7 @@ int check_device(DevInfo* di) {
 struct Plan {
   int variant = DWCONV_VARIANT_NONE;
   ChunkPlan chunk{};
+  NhwcPlan nhwc{};
 };
 
 // Choose the kernel family for a pass.  Pure host computation, memoised per
@@ -126,9 +128,16 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
     if (pass != DWCONV_PASS_BWD_FILTER || p->chunk.max_chain <= 160)
       p->variant = DWCONV_VARIANT_NCHW_CHUNK;
   }
+  if (g.layout == DWCONV_NHWC && dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->variant = DWCONV_VARIANT_NHWC_TILE;
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? DWCONV_OK : DWCONV_ERR_CUDA; }
+
+// the NHWC kernels move 4-channel vectors: 16-B (fp32) / 8-B (bf16) aligned activations
+bool nhwc_aligned(const Geom& g, const void* a, const void* b) {
+  const uintptr_t al = (g.dtype == DWCONV_F32) ? 16 : 8;
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % al) == 0;
+}
 
 }  // namespace
 
@@ -183,6 +192,8 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
   // the NCHW kernels store y with V-wide vector stores straight from registers
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(y) % 16) == 0)
     return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
+  if (p.variant == DWCONV_VARIANT_NHWC_TILE && nhwc_aligned(g, x, y))
+    return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_FWD, x, w, y, st));
   return cuda_status(dwk::launch_generic_fwd(g, x, w, y, st));
 }
 
@@ -203,6 +214,8 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
   // the NCHW kernels store dx with vector stores straight from registers
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0)
     return cuda_status(dwk::launch_nchw_bwd_data(g, p.chunk, dy, w, dx, st));
+  if (p.variant == DWCONV_VARIANT_NHWC_TILE && nhwc_aligned(g, dy, dx))
+    return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_BWD_DATA, dy, w, dx, st));
   return cuda_status(dwk::launch_generic_bwd_data(g, dy, w, dx, st));
 }
 
@@ -213,6 +226,7 @@ size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
   if (check_device(&di) != DWCONV_OK) return 0;
   Plan p;
   make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
+  if (p.variant == DWCONV_VARIANT_NHWC_TILE) return p.nhwc.ws_bytes;
   return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? p.chunk.ws_bytes : 0;
 }
 
@@ -240,6 +254,12 @@ int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float
     if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
     return cuda_status(dwk::launch_nchw_bwd_filter(g, p.chunk, x, dy, dw, workspace, st));
   }
+  if (p.variant == DWCONV_VARIANT_NHWC_TILE && nhwc_aligned(g, x, dy)) {
+    if (workspace_bytes < p.nhwc.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
+    if (!workspace) return DWCONV_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
+    return cuda_status(dwk::launch_nhwc_bwd_filter(g, p.nhwc, x, dy, dw, workspace, st));
+  }
   return cuda_status(dwk::launch_generic_bwd_filter(g, x, dy, dw, st));
 }
 
@@ -265,6 +285,11 @@ int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
     const ChunkPlan& c = p.chunk;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
     info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
+    info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+  } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
+    const NhwcPlan& c = p.nhwc;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
+    info->work_units = (pass == DWCONV_PASS_BWD_FILTER) ? (int64_t)c.groups * c.nslices : c.items;
     info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
   } else if (p.variant == DWCONV_VARIANT_GENERIC) {
     info->block = 256; info->launches = 1;

@@ -66,4 +66,21 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
 cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
                                    void* ws, cudaStream_t st);
 
+// ---- NHWC kernels (m = 1, 3x3, pad 1, S in {1,2}): nhwc.cu
+struct NhwcPlan {
+  int threads, grid, smem;
+  int TH, TW;             // fwd / bwd_data output tile; bwd_filter: dy columns per block
+  int OHB, OWB;           // tiles along output rows / columns
+  int64_t items;          // fwd / bwd_data work items (tile x channel vector)
+  int CVB, PSET;          // bwd_filter: channel vectors per CTA, pixel sets per channel vector
+  int groups, nslices, rps;
+  int max_chain;
+  size_t ws_bytes;
+};
+bool plan_nhwc(const Geom& g, int pass, int num_sms, NhwcPlan* plan);
+cudaError_t launch_nhwc_fd(const Geom& g, const NhwcPlan& p, int pass, const void* in, const void* w, void* out,
+                           cudaStream_t st);
+cudaError_t launch_nhwc_bwd_filter(const Geom& g, const NhwcPlan& p, const void* x, const void* dy, float* dw,
+                                   void* ws, cudaStream_t st);
+
 }  // namespace dwk

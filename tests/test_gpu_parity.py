@@ -222,3 +222,39 @@ def test_mobilenet_layers_random_fp32(_lib):
     import synth
     for L in synth.mobilenet_v1_dw(2):
         check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=NCHW, dtype="f32", kind="unif")
+
+
+# NHWC fast path (nhwc.cu): m = 1, 3x3, pad 1, C % 4 == 0 -- ragged tiles, several
+# channel-vector counts (grid-stride weight reuse, CV not dividing 256), s = 1, 2.
+NHWC_FAST = [
+    (2, 8, 16, 16, 1, 3, 1, 1),
+    (3, 12, 13, 11, 1, 3, 1, 1),    # CV = 3, ragged TH x TW tiles
+    (2, 24, 15, 9, 1, 3, 2, 1),     # CV = 6, stride 2, odd sizes
+    (1, 1028, 7, 7, 1, 3, 1, 1),    # CV = 257 > 256: two channel groups in bwd_filter
+    (2, 64, 28, 28, 1, 3, 2, 1),
+]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", NHWC_FAST)
+def test_nhwc_fast_path(shape, dtype, _lib):
+    import paper_1803_09926_b200.ops as ops
+    n, c, h, w, m, k, s, p = shape
+    d = ops.make_desc(n, c, h, w, m, k, s, p, NHWC, 0 if dtype == "f32" else 1)
+    for pas in (0, 1, 2):
+        assert ops.dwconv_plan(d, pas)["variant_name"] == "nhwc_tile", (shape, pas)
+    check_all(*shape, layout=NHWC, dtype=dtype, kind="unif")
+    check_all(*shape, layout=NHWC, dtype=dtype, kind="int", amax=2 if dtype == "bf16" else 3)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_mobilenet_layers_exact_nhwc(dtype, _lib):
+    """All 13 MobileNet-v1 layers in NHWC (configs[2] layout) through the NHWC kernels."""
+    import synth
+    import paper_1803_09926_b200.ops as ops
+    amax = 2 if dtype == "bf16" else 3
+    for L in synth.mobilenet_v1_dw(2):
+        d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, NHWC, 0 if dtype == "f32" else 1)
+        assert ops.dwconv_plan(d, 2)["variant_name"] == "nhwc_tile"
+        assert ops.dwconv_plan(d, 2)["max_chain"] <= 160
+        check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=NHWC, dtype=dtype, kind="int", amax=amax)
