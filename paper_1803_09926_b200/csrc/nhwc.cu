@@ -21,7 +21,7 @@
 //    (group of CVB channel vectors, slice of (n, oh) output rows); PSET pixel
 //    sets per channel vector each walk rows in TW-wide blocks.  Deterministic:
 //    per block (TW terms) -> running sum over the thread's blocks -> pixel sets
-//    in order (sequential) -> per-slice partials -> last CTA of the group sums
+//    pairwise in order -> per-slice partials -> last CTA of the group sums
 //    slices pairwise in slice order (integer ticket) and re-zeroes the workspace.
 #include <algorithm>
 #include <cstdlib>
@@ -244,8 +244,17 @@ __global__ void __launch_bounds__(256, 2) nhwc_bf_kernel(const HArgs a) {
     const int cl = e / (VC * KK);       // channel vector within the group
     const int rem = e - cl * VC * KK;   // q * VC + v
     const int q = rem / VC, v = rem - q * VC;
-    float s = red[cl * KK * VC + rem];
-    for (int p = 1; p < a.PSET; ++p) s += red[(p * a.CVB + cl) * KK * VC + rem];
+    // pixel sets in order, pairwise (binary counter): depth log2(PSET)
+    float stk[10];
+    int top = 0;
+    for (int p = 0; p < a.PSET; ++p) {
+      float cur = red[(p * a.CVB + cl) * KK * VC + rem];
+      int bits = p;
+      while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+      stk[top++] = cur;
+    }
+    float s = stk[--top];
+    while (top > 0) s = stk[--top] + s;
     part[(int64_t)((g * a.CVB + cl) * VC + v) * KK + q] = s;  // dw layout [c][tap]
   }
   __threadfence();
@@ -263,16 +272,16 @@ __global__ void __launch_bounds__(256, 2) nhwc_bf_kernel(const HArgs a) {
     for (int idx = threadIdx.x; idx < nvals; idx += blockDim.x) {
       float stk[16];
       int top = 0;
-      for (int s0 = 0; s0 < a.nslices; s0 += 8) {
-        float vals[8];
+      for (int s0 = 0; s0 < a.nslices; s0 += 32) {  // 32 loads in flight per thread
+        float vals[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 32; ++u)
           vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 32; ++u)
           if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 32; ++u) {
           const int s = s0 + u;
           if (s < a.nslices) {
             float cur = vals[u];
@@ -395,9 +404,11 @@ bool plan_nhwc(const Geom& g, int pass, int num_sms, NhwcPlan* p) {
   }
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem) != cudaSuccess || occ < 1) return false;
-  // slices: ~4 waves of CTAs, and <= 96 blocks per thread (running-sum chain)
-  int64_t nsl = std::max<int64_t>(1, ((int64_t)4 * occ * num_sms + groups - 1) / groups);
-  nsl = std::max<int64_t>(nsl, (rows * bpr + (int64_t)PSET * 96 - 1) / ((int64_t)PSET * 96));
+  // slices: ~one wave of CTAs (measured best: each CTA's epilogue is a fixed cost),
+  // and <= 120 blocks per thread (running-sum chain)
+  static const int waves = []() { const char* e = std::getenv("DWCONV_NHWC_BF_WAVES"); return e ? std::max(1, std::atoi(e)) : 1; }();
+  int64_t nsl = std::max<int64_t>(1, ((int64_t)waves * occ * num_sms + groups - 1) / groups);
+  nsl = std::max<int64_t>(nsl, (rows * bpr + (int64_t)PSET * 120 - 1) / ((int64_t)PSET * 120));
   nsl = std::min<int64_t>(nsl, std::min<int64_t>(rows, 256));
   const int64_t rps = (rows + nsl - 1) / nsl;
   nsl = (rows + rps - 1) / rps;
@@ -409,7 +420,9 @@ bool plan_nhwc(const Geom& g, int pass, int num_sms, NhwcPlan* p) {
   p->grid = (int)(groups * nsl);
   int lg = 0;
   while ((1ll << lg) < nsl) ++lg;
-  p->max_chain = (int)(TW + bpt + PSET + 2 * lg + 1);
+  int lp = 0;
+  while ((1 << lp) < PSET) ++lp;
+  p->max_chain = (int)(TW + bpt + lp + 2 * lg + 1);
   const size_t tick = ((size_t)groups * 4 + 15) / 16 * 16;
   p->ws_bytes = tick + (size_t)nsl * g.C * KK * 4;
   return p->max_chain <= 160 && p->grid > 0;

@@ -10,6 +10,7 @@ ap.add_argument("--layers", default="dw2,dw14,dw26")
 ap.add_argument("--passes", default="fwd,bwd_data,bwd_filter")
 ap.add_argument("--batches", default="16,64,256")
 ap.add_argument("--dtype", default="f32")
+ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"])
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--plan", action="store_true", help="append the chosen plan of the last batch")
 ap.add_argument("--flush-mb", type=int, default=256, help="bytes read between reps to evict L2 (keeps the GPU busy while the host enqueues)")
@@ -24,11 +25,13 @@ for lname in a.layers.split(","):
         row = []
         for n in [int(b) for b in a.batches.split(",")]:
             L = [l for l in synth.mobilenet_v1_dw(n) if l.name == lname][0]
-            d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, 0, 0 if a.dtype == "f32" else 1)
-            x = torch.randn(L.n, L.c, L.h, L.w, device="cuda").to(dt)
-            dy = torch.randn(L.n, L.c * L.m, L.ho, L.wo, device="cuda").to(dt)
+            lay = 0 if a.layout == "nchw" else 1
+            mf = torch.contiguous_format if lay == 0 else torch.channels_last
+            d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, lay, 0 if a.dtype == "f32" else 1)
+            x = torch.randn(L.n, L.c, L.h, L.w, device="cuda").to(dt).contiguous(memory_format=mf)
+            dy = torch.randn(L.n, L.c * L.m, L.ho, L.wo, device="cuda").to(dt).contiguous(memory_format=mf)
             w = torch.randn(L.c * L.m, L.k, L.k, device="cuda").to(dt)
-            y = torch.empty_like(dy); dx = torch.empty_like(x)
+            y = torch.empty_like(dy); dx = torch.empty_like(x)  # empty_like keeps the memory format
             dw = torch.empty(L.c * L.m, L.k, L.k, device="cuda")
             ws = torch.zeros(max(16, ops.dwconv_bwd_filter_workspace_bytes(d)), dtype=torch.uint8, device="cuda")
             f = {"fwd": lambda: ops.dwconv_fwd(d, x, w, y), "bwd_data": lambda: ops.dwconv_bwd_data(d, dy, w, dx),
