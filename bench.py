@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"])
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
     ap.add_argument("--serial", action="store_true", help="all 39 launches on one stream (no dgrad/wgrad overlap)")
+    ap.add_argument("--fused", default="none", choices=["none", "all", "small"],
+                    help="layers whose backward uses the fused dwconv_bwd (one pass over x and dy) instead of "
+                         "bwd_data + bwd_filter on two streams: none, all fusable, or the fusable 14x14/7x7 layers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -64,11 +67,13 @@ def workload_name(args):
     return w
 
 
-def step_bytes(layers, eb):
-    """Algorithmic HBM bytes of one fwd+bwd step: 3|x| + 3|y| + 3|w| + |dw|."""
+def step_bytes(layers, eb, fused=None):
+    """Algorithmic HBM bytes of one fwd+bwd step: 3|x| + 3|y| + 2|w| + |dw| per
+    layer; a layer whose backward is fused (dwconv_bwd, NEXT-1) reads dy once: 3|x| + 2|y| + ..."""
     tot = 0
-    for L in layers:
-        tot += 3 * L.x_elems() * eb + 3 * L.y_elems() * eb + 2 * L.w_elems() * eb + L.w_elems() * 4
+    for i, L in enumerate(layers):
+        ny = 2 if (fused and fused[i]) else 3
+        tot += 3 * L.x_elems() * eb + ny * L.y_elems() * eb + 2 * L.w_elems() * eb + L.w_elems() * 4
     return tot
 
 
@@ -77,6 +82,8 @@ def pass_bytes(L, pas, eb):
         return (L.x_elems() + L.y_elems() + L.w_elems()) * eb
     if pas == "bwd_data":
         return (L.x_elems() + L.y_elems() + L.w_elems()) * eb
+    if pas == "bwd":  # fused: x, dy, w read; dx, dw written
+        return (2 * L.x_elems() + L.y_elems() + L.w_elems()) * eb + L.w_elems() * 4
     return (L.x_elems() + L.y_elems()) * eb + L.w_elems() * 4
 
 
@@ -253,8 +260,19 @@ def main():
     def launch_bf(b):
         ops.dwconv_bwd_filter(b["d"], b["x"], b["dy"], b["dw"], ws)
 
-    kernels = [("fwd", b, launch_fwd) for b in bufs] + \
-              [(p, b, f) for b in reversed(bufs) for (p, f) in (("bwd_data", launch_bd), ("bwd_filter", launch_bf))]
+    # fused backward (dx + dw in one pass over x and dy) where the library has the kernel
+    for b in bufs:
+        b["fused"] = (args.fused == "all" or (args.fused == "small" and b["L"].h <= 14)) and \
+            ops.dwconv_plan(b["d"], 3)["variant_name"] != "none"
+    wsf = torch.zeros(max([16] + [ops.dwconv_bwd_workspace_bytes(b["d"]) for b in bufs if b["fused"]]),
+                      dtype=torch.uint8, device=dev)
+
+    def launch_bwd(b):
+        ops.dwconv_bwd(b["d"], b["x"], b["dy"], b["w"], b["dx"], b["dw"], wsf)
+
+    kernels = [("fwd", b, launch_fwd) for b in bufs]
+    for b in reversed(bufs):
+        kernels += [("bwd", b, launch_bwd)] if b["fused"] else [("bwd_data", b, launch_bd), ("bwd_filter", b, launch_bf)]
 
     side = torch.cuda.Stream(device=dev)
 
@@ -273,6 +291,9 @@ def main():
         for b in bufs:
             launch_fwd(b)
         for b in reversed(bufs):
+            if b["fused"]:
+                launch_bwd(b)
+                continue
             ev = torch.cuda.Event()
             ev.record(cur)
             side.wait_event(ev)
@@ -332,7 +353,7 @@ def main():
         ms = float(t.item())
     images = args.batch * world
     value = images / (ms / 1000.0)
-    sbytes = step_bytes(layers, eb)
+    sbytes = step_bytes(layers, eb, [b["fused"] for b in bufs])
     hbm_gbs = sbytes * world / (ms / 1000.0) / 1e9
 
     # ---- per-kernel durations (CUDA events around each launch, same order as the step)
@@ -353,7 +374,7 @@ def main():
         nbytes = pass_bytes(b["L"], pas, eb)
         kt.append(dict(layer=b["L"].name, pass_=pas, ms=mean_ms, bytes=nbytes, gbs=nbytes / (mean_ms * 1e-3) / 1e9))
         if args.extra:
-            pl = ops.dwconv_plan(b["d"], {"fwd": 0, "bwd_data": 1, "bwd_filter": 2}[pas])
+            pl = ops.dwconv_plan(b["d"], {"fwd": 0, "bwd_data": 1, "bwd_filter": 2, "bwd": 3}[pas])
             kt[-1]["plan"] = {k: pl[k] for k in ("variant_name", "grid", "block", "smem_bytes", "work_units",
                                                  "planes_per_chunk", "rows_per_band", "batch_slices")}
     kernel_sum_ms = sum(k["ms"] for k in kt)
@@ -376,8 +397,10 @@ def main():
         except Exception:
             traffic = None
     passes = {}
-    for pas in ("fwd", "bwd_data", "bwd_filter"):
+    for pas in ("fwd", "bwd_data", "bwd_filter", "bwd"):
         sel = [k for k in kt if k["pass_"] == pas]
+        if not sel:
+            continue
         pm = sum(k["ms"] for k in sel)
         pb = sum(k["bytes"] for k in sel)
         passes[pas] = {"ms": pm, "gbs": pb / (pm * 1e-3) / 1e9, "frac": pb / (pm * 1e-3) / 1e9 / peak}
@@ -441,7 +464,8 @@ def main():
                        "layers": 13, "layout": args.layout, "parallelism": f"dp{world}",
                        "l2": f"no flush: step footprint {footprint / 1e9:.2f} GB >> 126 MB L2",
                        "graph": graph is not None,
-                       "schedule": "serial" if args.serial else "bwd_filter on a side stream (overlaps bwd_data)"},
+                       "schedule": ("serial" if args.serial else "bwd_filter on a side stream (overlaps bwd_data)") +
+                                   f"; fused backward on {sum(b['fused'] for b in bufs)}/13 layers"},
             "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / world / peak,
             "algorithmic_bytes_per_step": sbytes * world,
             "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",

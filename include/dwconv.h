@@ -127,11 +127,30 @@ DWCONV_API size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d);
 DWCONV_API int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float* dw,
                       void* workspace, size_t workspace_bytes, dwconv_stream stream);
 
+/* Fused backward: dx = dwconv_transpose(dy, w) AND dw = sum of
+ * x (*) dy, from one pass over x and dy where a fused kernel exists (NCHW, 3x3,
+ * stride 1, pad 1, m = 1: dy is read from HBM once instead of twice, so the
+ * backward moves 2|x| + |dy| + ... instead of 2|x| + 2|dy|).  Other shapes run
+ * dwconv_bwd_data then dwconv_bwd_filter on the same stream.  Arguments as for
+ * those two calls (dx, dy: activations; w: [C*m][kh][kw]; dw: fp32 [C*m][kh][kw]);
+ * workspace: at least dwconv_bwd_workspace_bytes(d), same zero-fill contract as
+ * dwconv_bwd_filter.  Results equal the two-call results up to fp32 rounding
+ * order (dx is produced by the same stencil arithmetic; dw by the same fixed-order
+ * reduction scheme); bitwise reproducible run to run. */
+DWCONV_API size_t dwconv_bwd_workspace_bytes(const dwconv_desc* d);
+DWCONV_API int dwconv_bwd(const dwconv_desc* d, const void* x, const void* dy, const void* w, void* dx, float* dw,
+                          void* workspace, size_t workspace_bytes, dwconv_stream stream);
+
 /* Enqueue a zero-fill of a workspace (cudaMemsetAsync); needed once per buffer. */
 DWCONV_API int dwconv_workspace_init(void* workspace, size_t workspace_bytes, dwconv_stream stream);
 
 /* Diagnostics: which kernel family and launch shape a pass would use. */
-typedef enum { DWCONV_PASS_FWD = 0, DWCONV_PASS_BWD_DATA = 1, DWCONV_PASS_BWD_FILTER = 2 } dwconv_pass;
+typedef enum {
+  DWCONV_PASS_FWD = 0,
+  DWCONV_PASS_BWD_DATA = 1,
+  DWCONV_PASS_BWD_FILTER = 2,
+  DWCONV_PASS_BWD = 3  /* fused backward (dwconv_bwd); variant NONE with launches = 2: two-call fallback */
+} dwconv_pass;
 typedef enum {
   DWCONV_VARIANT_NONE = 0,        /* empty batch: nothing to launch (bwd_filter: a memset)  */
   DWCONV_VARIANT_GENERIC = 1,     /* any shape: one thread per output element, global loads */

@@ -13,10 +13,11 @@ LIB_PATH = os.path.join(_HERE, "libdwconv.so")
 
 NCHW, NHWC = 0, 1
 F32, BF16 = 0, 1
-PASS_FWD, PASS_BWD_DATA, PASS_BWD_FILTER = 0, 1, 2
+PASS_FWD, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_BWD = 0, 1, 2, 3
 VARIANTS = {0: "none", 1: "generic", 2: "nchw_chunk", 3: "nhwc_tile"}
 FUNCTIONS = ("dwconv_abi_version", "dwconv_status_string", "dwconv_output_shape", "dwconv_fwd",
              "dwconv_bwd_data", "dwconv_bwd_filter_workspace_bytes", "dwconv_bwd_filter",
+             "dwconv_bwd_workspace_bytes", "dwconv_bwd",
              "dwconv_workspace_init", "dwconv_plan", "dwconv_set_variant_override")
 
 
@@ -64,10 +65,13 @@ def load() -> ctypes.CDLL:
     lib.dwconv_bwd_filter_workspace_bytes.argtypes = [dp]
     lib.dwconv_bwd_filter_workspace_bytes.restype = sz
     lib.dwconv_bwd_filter.argtypes = [dp, vp, vp, vp, vp, sz, vp]
+    lib.dwconv_bwd_workspace_bytes.argtypes = [dp]
+    lib.dwconv_bwd_workspace_bytes.restype = sz
+    lib.dwconv_bwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.dwconv_workspace_init.argtypes = [vp, sz, vp]
     lib.dwconv_plan.argtypes = [dp, i32, ctypes.POINTER(PlanInfo)]
     lib.dwconv_set_variant_override.argtypes = [i32]
-    for f in ("dwconv_output_shape", "dwconv_fwd", "dwconv_bwd_data", "dwconv_bwd_filter",
+    for f in ("dwconv_output_shape", "dwconv_fwd", "dwconv_bwd_data", "dwconv_bwd_filter", "dwconv_bwd",
               "dwconv_workspace_init", "dwconv_plan", "dwconv_set_variant_override"):
         getattr(lib, f).restype = i32
     if lib.dwconv_abi_version() != 1:

@@ -1,5 +1,6 @@
 // host.cpp -- the C ABI of include/dwconv.h: validation, kernel-family
 // selection, launch.  No allocation, no synchronisation, no device switch.
+#include <algorithm>
 #include <array>
 #include <atomic>
 #include <map>
@@ -125,8 +126,12 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
   if (g.N == 0) { p->variant = DWCONV_VARIANT_NONE; return; }
   if (g_override.load() == DWCONV_VARIANT_GENERIC) return;
   if (g.layout == DWCONV_NCHW && dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &p->chunk)) {
-    if (pass != DWCONV_PASS_BWD_FILTER || p->chunk.max_chain <= 160)
+    if ((pass != DWCONV_PASS_BWD_FILTER && pass != DWCONV_PASS_BWD) || p->chunk.max_chain <= 160)
       p->variant = DWCONV_VARIANT_NCHW_CHUNK;
+  }
+  if (pass == DWCONV_PASS_BWD) {  // fused backward: NCHW chunk family, fp32 (bf16 measured slower fused)
+    if (p->variant != DWCONV_VARIANT_NCHW_CHUNK || g.dtype != DWCONV_F32) p->variant = DWCONV_VARIANT_NONE;
+    return;
   }
   if (g.layout == DWCONV_NHWC && dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->variant = DWCONV_VARIANT_NHWC_TILE;
 }
@@ -263,6 +268,43 @@ int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float
   return cuda_status(dwk::launch_generic_bwd_filter(g, x, dy, dw, st));
 }
 
+size_t dwconv_bwd_workspace_bytes(const dwconv_desc* d) {
+  Geom g;
+  if (validate(d, &g) != DWCONV_OK) return 0;
+  DevInfo di;
+  if (check_device(&di) != DWCONV_OK) return 0;
+  Plan p;
+  make_plan(g, DWCONV_PASS_BWD, di, &p);
+  const size_t two = dwconv_bwd_filter_workspace_bytes(d);
+  return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? std::max(p.chunk.ws_bytes, two) : two;
+}
+
+int dwconv_bwd(const dwconv_desc* d, const void* x, const void* dy, const void* w, void* dx, float* dw,
+               void* workspace, size_t workspace_bytes, dwconv_stream stream) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) ||
+      (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) || (s = check_ptr(dx, g.N * g.C * g.H * g.W, eb)) ||
+      (s = check_ptr(dw, g.C * g.m * g.kh * g.kw, 4)))
+    return s;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  Plan p;
+  if (g.N > 0) make_plan(g, DWCONV_PASS_BWD, di, &p);
+  // the fused kernel stores dx with vector stores straight from registers
+  if (g.N > 0 && p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0) {
+    if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
+    if (!workspace) return DWCONV_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return cuda_status(dwk::launch_nchw_bwd_fused(g, p.chunk, x, dy, w, dx, dw, workspace, st));
+  }
+  if ((s = dwconv_bwd_data(d, dy, w, dx, stream))) return s;
+  return dwconv_bwd_filter(d, x, dy, dw, workspace, workspace_bytes, stream);
+}
+
 int dwconv_workspace_init(void* workspace, size_t workspace_bytes, dwconv_stream stream) {
   if (workspace_bytes == 0) return DWCONV_OK;
   if (!workspace) return DWCONV_ERR_NULL_POINTER;
@@ -274,13 +316,18 @@ int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
   int s = validate(d, &g);
   if (s != DWCONV_OK) return s;
   if (!info) return DWCONV_ERR_NULL_POINTER;
-  if (pass < 0 || pass > 2) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (pass < 0 || pass > 3) return DWCONV_ERR_BAD_DESCRIPTOR;
   DevInfo di;
   if ((s = check_device(&di))) return s;
   Plan p;
   make_plan(g, pass, di, &p);
   std::memset(info, 0, sizeof(*info));
   info->variant = p.variant;
+  if (pass == DWCONV_PASS_BWD && p.variant != DWCONV_VARIANT_NCHW_CHUNK) {  // two-call fallback
+    info->variant = DWCONV_VARIANT_NONE;
+    info->launches = 2;
+    return DWCONV_OK;
+  }
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) {
     const ChunkPlan& c = p.chunk;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;

@@ -57,6 +57,8 @@ struct ChunkPlan {
   int dL, dSPW, dspc;   // lanes per row set, row sets per warp, row sets per channel
 };
 
+constexpr int kPassBwdFused = DWCONV_PASS_BWD;  // plan_nchw pass id of the fused backward
+
 // Returns false if the NCHW chunk family cannot handle the geometry.
 bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
@@ -65,6 +67,8 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
                                  cudaStream_t st);
 cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
                                    void* ws, cudaStream_t st);
+cudaError_t launch_nchw_bwd_fused(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, const void* w,
+                                  void* dx, float* dw, void* ws, cudaStream_t st);
 
 // ---- NHWC kernels (m = 1, 3x3, pad 1, S in {1,2}): nhwc.cu
 struct NhwcPlan {

@@ -17,7 +17,12 @@ namespace dwk {
 namespace nchw {
 namespace {
 
-template <class T, int K, int S, int R, int V, bool PADDED>
+// FUSED (S = 1, m = 1): the fused backward.  The dy planes are
+// staged with PAD halo rows, and every thread strip also computes the matching
+// R x V strip of dx -- the forward stencil over the staged dy with the flipped
+// kernel (reading R9) -- and stores it, so dy is read from HBM once for both
+// gradients: 3|x| + 2|y| per layer instead of 3|x| + 3|y|.
+template <class T, int K, int S, int R, int V, bool PADDED, bool FUSED = false>
 __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int NRows = (R - 1) * S + K;
@@ -43,7 +48,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   auto sx_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
   auto sdy_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + a.in2_off + st * a.in_stage); };
 
-  struct Rows { int64_t n; int r0, r1, lo, hi; };
+  struct Rows { int64_t n; int r0, r1, lo, hi, dlo, dhi; };  // dy rows [r0,r1) staged as [dlo,dhi); x rows [lo,hi)
   auto rows_of = [&](int kk) {
     Rows r;
     const int nn = kk / a.nbands;
@@ -56,10 +61,12 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
       r.lo = max(0, r.r0 * S - PAD);
       r.hi = min(H, (r.r1 - 1) * S - PAD + K);
     }
+    r.dlo = FUSED ? max(0, r.r0 - PAD) : r.r0;  // fused: dy halo rows for the dx stencil
+    r.dhi = FUSED ? min(Ho, r.r1 + PAD) : r.r1;
     return r;
   };
   auto x_src = [&](const Rows& r) { return x + ((r.n * a.C + c0ch) * H + r.lo) * W; };
-  auto dy_src = [&](const Rows& r) { return dy + (((r.n * a.C + c0ch) * m) * Ho + r.r0) * Wo; };
+  auto dy_src = [&](const Rows& r) { return dy + (((r.n * a.C + c0ch) * m) * Ho + r.dlo) * Wo; };
   auto x_spec = [&](const Rows& r) {
     StageSpec sp;
     sp.cnt = (int64_t)(r.hi - r.lo) * W;
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   };
   auto dy_spec = [&](const Rows& r) {  // dy needs no halo: planes back to back
     StageSpec sp;
-    sp.cnt = (int64_t)(r.r1 - r.r0) * Wo;
+    sp.cnt = (int64_t)(r.dhi - r.dlo) * Wo;
     sp.gstride = (int64_t)Ho * Wo;
     sp.npl = np * m;
     sp.pitch = (int)sp.cnt;
@@ -100,6 +107,13 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   float run[KK];
 #pragma unroll
   for (int q = 0; q < KK; ++q) run[q] = 0.f;
+  float wf[FUSED ? KK : 1];  // fused: this plane's kernel, flipped (dx = forward stencil of dy)
+  if constexpr (FUSED) {
+    const T* wt = static_cast<const T*>(a.w);
+    const int o = c0ch * m + (active ? gp : 0);
+#pragma unroll
+    for (int q = 0; q < KK; ++q) wf[q] = Elem<T>::ldg(wt + (int64_t)o * KK + (KK - 1 - q));
+  }
 
   if (threadIdx.x == 0)
     for (int i = 0; i < a.ns - 1 && i < iters; ++i) issue(i, i);
@@ -121,9 +135,9 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     __syncthreads();
     if (active) {
       const int rows_x = r.hi - r.lo;
-      const int rows_dy = r.r1 - r.r0;
+      const int rows_dy = r.dhi - r.dlo;
       const T* s_x = sx + (gp / m) * xs.pitch + xs.zbe - r.lo * W;  // row ih at s_x + ih * W
-      const T* s_dy = sdy + gp * rows_dy * Wo - r.r0 * Wo;  // row oh at s_dy + oh * Wo
+      const T* s_dy = sdy + gp * rows_dy * Wo - r.dlo * Wo;  // row oh at s_dy + oh * Wo
       float2 loc2[kPacked ? KK : 1];
       float loc[kPacked ? 1 : KK];
 #pragma unroll
@@ -177,6 +191,18 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
               }
             }
           }
+        }
+        if constexpr (FUSED) {  // dx strip at the same rows / columns (S = 1: H = Ho, W = Wo)
+          float acc[R][V];
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+            for (int u = 0; u < V; ++u) acc[tt][u] = 0.f;
+          stencil_strip<T, K, 1, R, V, false>(s_dy, zrow, Wo, r.dlo, rows_dy, oh0 - PAD, c0, wf, acc);
+          T* xo = static_cast<T*>(a.out) + ((r.n * a.C + c0ch + gp) * (int64_t)H + oh0) * W + c0;
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt)
+            if (oh0 + tt < r.r1) VecIO<T, V>::store(xo + (int64_t)tt * W, acc[tt]);
         }
       }
 #pragma unroll
@@ -293,6 +319,33 @@ KernelFn pick_t(int K, int S, int RI, int VI) {
 }
 
 }  // namespace
+
+// Fused backward (3x3, S = 1, m = 1): V in {1, 2, 4}.
+template <class T, bool PD>
+KernelFn pick_fused(int RI, int VI) {
+  constexpr int R0 = rows_bf(3, 0), R1 = rows_bf(3, 1);
+  switch (VI) {
+    case 0: return RI == 0 ? nchw_bwd_filter_kernel<T, 3, 1, R0, 1, PD, true> : nchw_bwd_filter_kernel<T, 3, 1, R1, 1, PD, true>;
+    case 1: return RI == 0 ? nchw_bwd_filter_kernel<T, 3, 1, R0, 2, PD, true> : nchw_bwd_filter_kernel<T, 3, 1, R1, 2, PD, true>;
+    case 2:
+      if constexpr (PD)
+        return RI == 0 ? nchw_bwd_filter_kernel<T, 3, 1, R0, 4, PD, true> : nchw_bwd_filter_kernel<T, 3, 1, R1, 4, PD, true>;
+      else
+        return nullptr;
+    case 3:
+      if constexpr (PD && std::is_same<T, __nv_bfloat16>::value)
+        return RI == 0 ? nchw_bwd_filter_kernel<T, 3, 1, R0, 8, PD, true> : nchw_bwd_filter_kernel<T, 3, 1, R1, 8, PD, true>;
+      else
+        return nullptr;
+    default: return nullptr;
+  }
+}
+
+KernelFn bwd_fused_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
+  if (K != 3 || S != 1) return nullptr;
+  if (dtype == DWCONV_F32) return padded ? pick_fused<float, true>(RI, VI) : pick_fused<float, false>(RI, VI);
+  return padded ? pick_fused<__nv_bfloat16, true>(RI, VI) : pick_fused<__nv_bfloat16, false>(RI, VI);
+}
 
 KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
   if (dtype == DWCONV_F32) return padded ? pick_t<float, true>(K, S, RI, VI) : pick_t<float, false>(K, S, RI, VI);

@@ -59,6 +59,7 @@ using KernelFn = void (*)(NArgs);
 KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
 KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
 KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
+KernelFn bwd_fused_kernel(int dtype, int K, int S, int RI, int VI, bool padded);  // dx + dw in one pass
 
 // Strip heights: index 0 = "7*2^k planes", index 1 = default.
 __host__ __device__ constexpr int rows_fwd(int K, int RI) { return K == 3 ? (RI == 0 ? 7 : 8) : (K == 5 ? 8 : 4); }

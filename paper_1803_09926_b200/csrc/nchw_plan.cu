@@ -88,6 +88,7 @@ int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb, int K) {
 KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded) {
   if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI, padded);
   if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded);
+  if (pass == kPassBwdFused) return bwd_fused_kernel(dtype, K, S, RI, VI, padded);
   return bwd_filter_kernel(dtype, K, S, RI, VI, padded);
 }
 
@@ -352,8 +353,10 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     return true;
   }
 
-  // ---------------- bwd_filter
-  if (plan_direct_bwd_filter(g, num_sms, p)) return true;
+  // ---------------- bwd_filter (and the fused backward: + dx from the same staged dy)
+  const bool fused = pass == kPassBwdFused;
+  if (fused && (g.m != 1 || S != 1 || K != 3)) return false;
+  if (!fused && plan_direct_bwd_filter(g, num_sms, p)) return true;
   const int64_t per = x_plane + y_plane;
   p->ri = (g.Ho % rows_bf(K, 0) == 0) ? 0 : 1;
   p->R = rows_bf(K, p->ri);
@@ -415,7 +418,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     for (int nsb_b = 1; nsb_b <= nsb_full; ++nsb_b) {
       const int br = nsb_b * R;
       const int64_t xb = std::min<int64_t>(g.H, (int64_t)(br - 1) * S + K) * g.W * eb;
-      const int64_t dyb = (int64_t)m * br * g.Wo * eb;
+      const int64_t dyb = (int64_t)m * std::min<int64_t>(g.Ho, br + (fused ? 2 * PADr : 0)) * g.Wo * eb;
       if (xb + dyb > budget_max) break;
       const int nb = (nsb_full + nsb_b - 1) / nsb_b;
       for (int tpg = 1; m * tpg <= kThreads; ++tpg) consider(1, tpg, nb, br, xb, dyb);
@@ -559,6 +562,18 @@ cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void
   a.ws_ticket = static_cast<unsigned*>(ws);
   a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   nchw::KernelFn fn = nchw::bwd_filter_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  return launch(fn, p, st, a);
+}
+
+cudaError_t launch_nchw_bwd_fused(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, const void* w,
+                                  void* dx, float* dw, void* ws, cudaStream_t st) {
+  nchw::NArgs a = base_args(g, p);
+  a.in = x; a.in2 = dy; a.dw = dw; a.w = w; a.out = dx;
+  const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
+  a.ws_ticket = static_cast<unsigned*>(ws);
+  a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
+  nchw::KernelFn fn = nchw::bwd_fused_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  if (!fn) return cudaErrorInvalidValue;
   return launch(fn, p, st, a);
 }
 

@@ -110,6 +110,21 @@ def dwconv_bwd_filter(d: Desc, x: torch.Tensor, dy: torch.Tensor, dw: torch.Tens
                                              nbytes, _stream(stream)), "dwconv_bwd_filter")
 
 
+def dwconv_bwd_workspace_bytes(d: Desc) -> int:
+    return int(_lib.load().dwconv_bwd_workspace_bytes(ctypes.byref(d)))
+
+
+def dwconv_bwd(d: Desc, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, dw: torch.Tensor,
+               workspace: Optional[torch.Tensor], stream=None) -> None:
+    """Fused backward: dx and dw from one pass over x and dy where the library has a fused kernel."""
+    _check_dev(x, dy, w, dx, dw)
+    if dw.dtype != torch.float32:
+        raise TypeError("dw is always float32")
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _lib.check(_lib.load().dwconv_bwd(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(w), _ptr(dx), _ptr(dw),
+                                      _ptr(workspace), nbytes, _stream(stream)), "dwconv_bwd")
+
+
 def dwconv_workspace_init(workspace: torch.Tensor, stream=None) -> None:
     _lib.check(_lib.load().dwconv_workspace_init(_ptr(workspace), workspace.numel() * workspace.element_size(),
                                                  _stream(stream)), "dwconv_workspace_init")
@@ -203,6 +218,17 @@ def bwd_filter(x: torch.Tensor, dy: torch.Tensor, w_shape: Sequence[int], stride
     return dw
 
 
+def bwd(x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, stride: IntPair = 1, padding: IntPair = 0,
+        layout: Optional[int] = None):
+    """(dx, dw) of one layer through the fused backward entry point (dwconv_bwd)."""
+    d = desc_for(x, w.shape, stride, padding, layout)
+    dx = _alloc((d.n, d.c, d.h, d.w), x, d.layout)
+    dw = torch.empty((d.c * d.multiplier, d.kh, d.kw), dtype=torch.float32, device=x.device)
+    ws = WORKSPACES.get(dwconv_bwd_workspace_bytes(d), x.device)
+    dwconv_bwd(d, x, dy, w.contiguous(), dx, dw, ws)
+    return dx, dw
+
+
 class DepthwiseConv2dFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, stride, padding):
@@ -218,6 +244,9 @@ class DepthwiseConv2dFn(torch.autograd.Function):
         mf = torch.channels_last if lay == NHWC else torch.contiguous_format
         dy = dy.contiguous(memory_format=mf)
         dx = dw = None
+        if ctx.needs_input_grad[0] and ctx.needs_input_grad[1]:  # one fused pass over x and dy
+            dx, dw = bwd(x, dy, w3, ctx.stride, ctx.padding, lay)
+            return dx, dw.to(w3.dtype).reshape(ctx.wshape), None, None
         if ctx.needs_input_grad[0]:
             dx = bwd_data(dy, w3, x.shape, ctx.stride, ctx.padding, lay)
         if ctx.needs_input_grad[1]:

@@ -258,3 +258,72 @@ def test_mobilenet_layers_exact_nhwc(dtype, _lib):
         assert ops.dwconv_plan(d, 2)["variant_name"] == "nhwc_tile"
         assert ops.dwconv_plan(d, 2)["max_chain"] <= 160
         check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=NHWC, dtype=dtype, kind="int", amax=amax)
+
+
+# Fused backward (dwconv_bwd): NCHW 3x3 s=1 m=1 shapes take one
+# kernel that produces dx and dw from a single pass over x and dy.
+FUSED_SHAPES = [
+    (2, 8, 16, 16, 1, 3, 1, 1),
+    (3, 5, 13, 11, 1, 3, 1, 1),     # ragged, W not a multiple of 4
+    (2, 3, 80, 80, 1, 3, 1, 1),     # band mode: dy halo rows staged per band
+    (3, 40, 7, 7, 1, 3, 1, 1),
+    (2, 6, 14, 14, 1, 3, 1, 1),
+]
+
+
+def _run_fused(inp, s, p, dtype):
+    import paper_1803_09926_b200 as dwl
+    x = to_dev(inp["x"], NCHW, dtype)
+    w = to_dev(inp["w"], NCHW, dtype)
+    dy = to_dev(inp["dy"], NCHW, dtype)
+    dx, dw = dwl.bwd(x, dy, w, s, p)
+    dx2 = dwl.bwd_data(dy, w, x.shape, s, p)
+    torch.cuda.synchronize()
+    return dx, dw, dx2
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", FUSED_SHAPES)
+def test_fused_backward(shape, dtype, _lib):
+    import paper_1803_09926_b200.ops as ops
+    from gpu_util import to_np
+    n, c, h, w, m, k, s, p = shape
+    d = ops.make_desc(n, c, h, w, m, k, s, p, NCHW, 0 if dtype == "f32" else 1)
+    # fused kernel for fp32; bf16 takes the two-call path (measured faster)
+    assert ops.dwconv_plan(d, 3)["variant_name"] == ("nchw_chunk" if dtype == "f32" else "none"), shape
+    if dtype == "f32":
+        assert ops.dwconv_plan(d, 3)["max_chain"] <= 160
+    for kind in ("unif", "int"):
+        inp = make_inputs(*shape, kind=kind, dtype=dtype, amax=2 if dtype == "bf16" else 3)
+        dx, dwv, dx_two = _run_fused(inp, s, p, dtype)
+        _, (rdx, adx), (rdw, adw) = run_oracle(inp, s, p)
+        check_close(to_np(dx), rdx, adx, dtype, "fused dx", kind == "int")
+        check_close(to_np(dwv), rdw, adw, "f32", "fused dw", kind == "int")
+        # dx comes from the same stencil arithmetic as dwconv_bwd_data (tap order per output)
+        assert torch.equal(dx, dx_two), shape
+
+
+def test_fused_backward_fallback_and_layers(_lib):
+    """Shapes without a fused kernel fall back to the two calls; the MobileNet
+    stride-1 layers all fuse (batch 2, exact on integers)."""
+    import synth
+    import paper_1803_09926_b200.ops as ops
+    from gpu_util import to_np
+    d = ops.make_desc(2, 4, 9, 9, 2, 3, 1, 1, NCHW, 0)  # m = 2: fallback
+    info = ops.dwconv_plan(d, 3)
+    assert info["variant_name"] == "none" and info["launches"] == 2
+    inp = make_inputs(2, 4, 9, 9, 2, 3, 1, 1, kind="int")
+    dx, dwv, _ = _run_fused(inp, 1, 1, "f32")
+    _, (rdx, adx), (rdw, adw) = run_oracle(inp, 1, 1)
+    check_close(to_np(dx), rdx, adx, "f32", "fallback dx", True)
+    check_close(to_np(dwv), rdw, adw, "f32", "fallback dw", True)
+    for L in synth.mobilenet_v1_dw(2):
+        if L.s != 1:
+            continue
+        d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, NCHW, 0)
+        assert ops.dwconv_plan(d, 3)["variant_name"] == "nchw_chunk", L
+        inp = make_inputs(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, kind="int")
+        dx, dwv, _ = _run_fused(inp, L.s, L.p, "f32")
+        _, (rdx, adx), (rdw, adw) = run_oracle(inp, L.s, L.p)
+        check_close(to_np(dx), rdx, adx, "f32", "fused dx", True)
+        check_close(to_np(dwv), rdw, adw, "f32", "fused dw", True)

@@ -17,6 +17,7 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--only", default="")
+ap.add_argument("--fused", action="store_true", help="use dwconv_bwd for layers that have a fused kernel")
 a = ap.parse_args()
 dt = torch.float32 if a.dtype == "f32" else torch.bfloat16
 eb = 4 if a.dtype == "f32" else 2
@@ -31,11 +32,17 @@ for L in layers:
     b["y"] = torch.empty_like(b["dy"]); b["dx"] = torch.empty_like(b["x"])
     b["dw"] = torch.empty(L.c * L.m, L.k, L.k, device="cuda")
     b["ws"] = torch.zeros(max(16, ops.dwconv_bwd_filter_workspace_bytes(d)), dtype=torch.uint8, device="cuda")
+    b["wsf"] = torch.zeros(max(16, ops.dwconv_bwd_workspace_bytes(d)), dtype=torch.uint8, device="cuda")
+    b["fused"] = a.fused and ops.dwconv_plan(d, 3)["variant_name"] != "none"
     bufs.append(b)
 for b in bufs:
     launches.append((b["L"].name, "fwd", (b["x"].numel() + b["y"].numel()) * eb,
                      lambda b=b: ops.dwconv_fwd(b["d"], b["x"], b["w"], b["y"])))
 for b in reversed(bufs):
+    if b["fused"]:
+        launches.append((b["L"].name, "bwd", (2 * b["x"].numel() + b["y"].numel()) * eb,
+                         lambda b=b: ops.dwconv_bwd(b["d"], b["x"], b["dy"], b["w"], b["dx"], b["dw"], b["wsf"])))
+        continue
     launches.append((b["L"].name, "bwd_data", (b["x"].numel() + b["y"].numel()) * eb,
                      lambda b=b: ops.dwconv_bwd_data(b["d"], b["dy"], b["w"], b["dx"])))
     launches.append((b["L"].name, "bwd_filter", (b["x"].numel() + b["y"].numel()) * eb,

@@ -34,8 +34,10 @@ for lname in a.layers.split(","):
             y = torch.empty_like(dy); dx = torch.empty_like(x)  # empty_like keeps the memory format
             dw = torch.empty(L.c * L.m, L.k, L.k, device="cuda")
             ws = torch.zeros(max(16, ops.dwconv_bwd_filter_workspace_bytes(d)), dtype=torch.uint8, device="cuda")
+            wsf = torch.zeros(max(16, ops.dwconv_bwd_workspace_bytes(d)), dtype=torch.uint8, device="cuda")
             f = {"fwd": lambda: ops.dwconv_fwd(d, x, w, y), "bwd_data": lambda: ops.dwconv_bwd_data(d, dy, w, dx),
-                 "bwd_filter": lambda: ops.dwconv_bwd_filter(d, x, dy, dw, ws)}[pas]
+                 "bwd_filter": lambda: ops.dwconv_bwd_filter(d, x, dy, dw, ws),
+                 "bwd": lambda: ops.dwconv_bwd(d, x, dy, w, dx, dw, wsf)}[pas]
             for _ in range(3): f()
             if a.graph:
                 torch.cuda.synchronize()
@@ -52,11 +54,11 @@ for lname in a.layers.split(","):
                 times.append(e0.elapsed_time(e1) * 1e3)
             times.sort()
             us = times[len(times) // 2]
-            nbytes = (L.x_elems() + L.y_elems()) * eb
+            nbytes = (L.x_elems() + L.y_elems()) * eb * (2 if pas == "bwd" else 1) - (L.y_elems() * eb if pas == "bwd" else 0)
             row.append((n, round(us, 2), round(nbytes / us / 1e3)))
         extra = ""
         if a.plan:
-            pi = ops.dwconv_plan(d, {"fwd": 0, "bwd_data": 1, "bwd_filter": 2}[pas])
+            pi = ops.dwconv_plan(d, {"fwd": 0, "bwd_data": 1, "bwd_filter": 2, "bwd": 3}[pas])
             extra = " ".join(f"{k}={pi[k]}" for k in ("variant_name", "grid", "block", "smem_bytes", "planes_per_chunk",
                                                       "rows_per_band", "batch_slices"))
         print(lname, pas, row, extra, flush=True)
