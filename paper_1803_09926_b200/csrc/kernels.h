@@ -31,6 +31,7 @@ struct ChunkPlan {
   int R;                // strip height (output rows per thread strip)
   int vi, V;            // column-vector variant: V = 1 << vi output columns per thread strip
   bool padded;          // input planes staged with zero rows around them
+  bool pair;            // fwd bf16: strips of two planes at once (FFMA2 lanes = planes)
   int pitch, zbe;       // padded staging: elements between planes, zero elements above a plane
   int ncg;              // column groups (strips across a row)
   int nsb;              // strips down a band

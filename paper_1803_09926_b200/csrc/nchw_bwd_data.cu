@@ -107,6 +107,10 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
       if (threadIdx.x == 0) mbar_arrive(&full[s]);  // second arrival: the weight table is written
       if (++s == a.ns) { s = 0; ph ^= 1; }
     }
+    // every load of this CTA is issued: let the next kernel on the stream launch
+    // and run its prologue on free SM resources (it still waits for this grid to
+    // complete in griddepcontrol.wait before touching global memory)
+    if (a.early_pdl) griddep_launch_dependents();
   } else {
     // ------------------------------------------------------------ consumers
     const int ctid = threadIdx.x - 32;

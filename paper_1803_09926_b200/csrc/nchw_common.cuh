@@ -49,6 +49,7 @@ struct NArgs {
   FastDiv div_c, div_nb;  // channel of a plane index; chunk -> (plane, band)
   int wbulk;              // w is 16-B aligned with a 16-B multiple size: weight rows may be bulk-copied
   int dbg;                // tuning aid (DWCONV_DEBUG): 1 = skip compute, 2 = skip stores
+  int early_pdl;          // persistent kernels: trigger the dependent launch once the producer is done
 };
 
 using KernelFn = void (*)(NArgs);
@@ -56,7 +57,7 @@ using KernelFn = void (*)(NArgs);
 // Kernel tables (one per pass, each in its own translation unit).
 // RI: strip-height variant, VI: column-vector variant (V = 1 << VI).
 // PADDED: input planes staged with zero rows around them (see stage_issue).
-KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
+KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false);
 KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
 KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
 KernelFn bwd_fused_kernel(int dtype, int K, int S, int RI, int VI, bool padded);  // dx + dw in one pass
@@ -376,6 +377,94 @@ __device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, i
             for (int u = 0; u < V; ++u) acc[tt][u] = fmaf(w, xw[S * u + jj], acc[tt][u]);
           }
         }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bf16 plane pairs
+// bf16 strips of TWO planes at once: packed FFMA2 lanes = (plane A, plane B) at
+// the same position, so every operand pair is built straight from the loaded
+// 16-bit values (one shift or mask per element into the pair's register) and no
+// column pair ever straddles registers -- no pair-forming moves, FFMA2 at any
+// stride.  Window: columns [S*c0 - PAD, S*c0 - PAD + (V-1)*S + K), as Win<K,S,V>.
+__device__ __forceinline__ float bf_bits_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_bits_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+template <int NW>
+__device__ __forceinline__ void load_words(const __nv_bfloat16* p, uint32_t* w) {
+  if constexpr (NW == 1) {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else if constexpr (NW == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    w[0] = v.x; w[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < NW / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[q];
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  }
+}
+template <int K, int S, int V>
+__device__ __forceinline__ void load_window_pair(const __nv_bfloat16* pa, const __nv_bfloat16* pb, const bool* lok,
+                                                 const bool* rok, float2* xw) {
+  using Wd = Win<K, S, V>;
+  static_assert(Wd::NV % 2 == 0, "pair windows load whole 32-bit words");
+  constexpr int NW = Wd::NV / 2;
+  uint32_t wa[NW], wb[NW];
+  load_words<NW>(pa, wa);
+  load_words<NW>(pb, wb);
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    xw[Wd::NL + 2 * k] = make_float2(bf_bits_lo(wa[k]), bf_bits_lo(wb[k]));
+    xw[Wd::NL + 2 * k + 1] = make_float2(bf_bits_hi(wa[k]), bf_bits_hi(wb[k]));
+  }
+  const unsigned short* ua = reinterpret_cast<const unsigned short*>(pa);
+  const unsigned short* ub = reinterpret_cast<const unsigned short*>(pb);
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l)
+    xw[l] = lok[l] ? make_float2(bf_bits_lo(ua[l - Wd::NL]), bf_bits_lo(ub[l - Wd::NL])) : make_float2(0.f, 0.f);
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r)
+    xw[Wd::NL + Wd::NV + r] =
+        rok[r] ? make_float2(bf_bits_lo(ua[Wd::NV + r]), bf_bits_lo(ub[Wd::NV + r])) : make_float2(0.f, 0.f);
+}
+// acc[tt][u] = (plane A, plane B) sums of stencil_strip at the same position.
+template <int K, int S, int R, int V, bool PADDED>
+__device__ __forceinline__ void stencil_strip_pair(const __nv_bfloat16* spa, const __nv_bfloat16* spb,
+                                                   const __nv_bfloat16* zp, int W, int lo, int rows, int ih0, int c0,
+                                                   const float2* wp, float2 (&acc)[R][V]) {
+  using Wd = Win<K, S, V>;
+  constexpr int NRows = (R - 1) * S + K;
+  const int b0 = S * c0;
+  bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r) rok[r] = b0 + Wd::NV + r < W;
+  const __nv_bfloat16* pra = spa + ih0 * W + b0;
+  const __nv_bfloat16* prb = spb + ih0 * W + b0;
+#pragma unroll
+  for (int r = 0; r < NRows; ++r) {
+    const __nv_bfloat16 *pa, *pb;
+    if constexpr (PADDED) {
+      pa = pra + r * W;
+      pb = prb + r * W;
+    } else {
+      const bool rv = (unsigned)(ih0 + r - lo) < (unsigned)rows;
+      pa = rv ? pra + r * W : zp + b0;
+      pb = rv ? prb + r * W : zp + b0;
+    }
+    float2 xw[Wd::N];
+    load_window_pair<K, S, V>(pa, pb, lok, rok, xw);
+#pragma unroll
+    for (int tt = 0; tt < R; ++tt) {
+      const int i = r - tt * S;
+      if (i >= 0 && i < K) {
+#pragma unroll
+        for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+          for (int u = 0; u < V; ++u) acc[tt][u] = __ffma2_rn(wp[i * K + jj], xw[S * u + jj], acc[tt][u]);
       }
     }
   }

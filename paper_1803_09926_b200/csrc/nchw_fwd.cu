@@ -39,7 +39,9 @@ __device__ __forceinline__ ChunkRows fwd_rows(const NArgs& a, int64_t c) {
   return k;
 }
 
-template <class T, int K, int S, int R, int V, bool PADDED>
+// PAIR (bf16): consumers compute strips of two output planes at once
+// (stencil_strip_pair): FFMA2 lanes = planes, no pair-forming moves.
+template <class T, int K, int S, int R, int V, bool PADDED, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -102,6 +104,10 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
       if (threadIdx.x == 0) mbar_arrive(&full[s]);  // second arrival: the weight table is written
       if (++s == a.ns) { s = 0; ph ^= 1; }
     }
+    // every load of this CTA is issued: let the next kernel on the stream launch
+    // and run its prologue on free SM resources (it still waits for this grid to
+    // complete in griddepcontrol.wait before touching global memory)
+    if (a.early_pdl) griddep_launch_dependents();
   } else {
     // ------------------------------------------------------------ consumers
     const int ctid = threadIdx.x - 32;
@@ -126,7 +132,50 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
       const float* swc = sw_of(s);
       const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
       const T* swr = reinterpret_cast<const T*>(swc) + ww.off;  // raw rows (ww.tma)
-      const int ntiles = (a.dbg & 1) ? 0 : npl * a.nsb * ncg;
+      if constexpr (PAIR) {
+        const int npair = (npl + 1) >> 1;
+        const int ntp = (a.dbg & 1) ? 0 : npair * a.nsb * ncg;
+        for (int t = ctid; t < ntp; t += nct) {
+          const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
+          const int c0 = (t - t2 * ncg) * V;
+          const int pp2 = (int)fdiv((uint32_t)t2, a.div_nsb);
+          const int sb = t2 - pp2 * a.nsb;
+          const int ppa = 2 * pp2;
+          const bool hasb = ppa + 1 < npl;
+          const int ppb = hasb ? ppa + 1 : ppa;
+          const int pina = (int)fdiv((uint32_t)ppa, a.div_m), pinb = (int)fdiv((uint32_t)ppb, a.div_m);
+          const int oh0 = k.r0 + sb * R;
+          float2 wp[KK];
+          if (ww.tma) {
+#pragma unroll
+            for (int q = 0; q < KK; ++q) wp[q] = make_float2(Elem<T>::load(swr + ppa * KK + q), Elem<T>::load(swr + ppb * KK + q));
+          } else {
+#pragma unroll
+            for (int q = 0; q < KK; ++q) wp[q] = make_float2(swc[ppa * KK + q], swc[ppb * KK + q]);
+          }
+          float2 acc[R][V];
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+            for (int u = 0; u < V; ++u) acc[tt][u] = make_float2(0.f, 0.f);
+          const T* base = sin + sp.zbe - k.lo * W;
+          stencil_strip_pair<K, S, R, V, PADDED>(base + pina * sp.pitch, base + pinb * sp.pitch, zrow, W, k.lo, rows_in,
+                                                 oh0 * S - PAD, c0, wp, acc);
+          T* yoa = y + ((k.q0 * m + ppa) * a.Ho + oh0) * Wo + c0;
+          T* yob = yoa + (int64_t)a.Ho * Wo;
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt) {
+            if (oh0 + tt < k.r1 && !(a.dbg & 2)) {
+              float va[V], vb[V];
+#pragma unroll
+              for (int u = 0; u < V; ++u) { va[u] = acc[tt][u].x; vb[u] = acc[tt][u].y; }
+              VecIO<T, V>::store(yoa + tt * Wo, va);
+              if (hasb) VecIO<T, V>::store(yob + tt * Wo, vb);
+            }
+          }
+        }
+      }
+      const int ntiles = ((a.dbg & 1) || PAIR) ? 0 : npl * a.nsb * ncg;
       for (int t = ctid; t < ntiles; t += nct) {
         const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
         const int c0 = (t - t2 * ncg) * V;
@@ -197,7 +246,30 @@ KernelFn pick_t(int K, int S, int RI, int VI) {
 
 }  // namespace
 
-KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
+// bf16 plane-pair kernels: S*V even (whole 32-bit words per window), 3x3.
+template <int S, int R, bool PD>
+KernelFn pick_pair_v(int VI) {
+  using B = __nv_bfloat16;
+  switch (VI) {
+    case 0: if constexpr (S == 2) return nchw_fwd_kernel<B, 3, S, R, 1, PD, true>; else return nullptr;
+    case 1: return nchw_fwd_kernel<B, 3, S, R, 2, PD, true>;
+    case 2: if constexpr (PD) return nchw_fwd_kernel<B, 3, S, R, 4, PD, true>; else return nullptr;
+    case 3: if constexpr (PD) return nchw_fwd_kernel<B, 3, S, R, 8, PD, true>; else return nullptr;
+    default: return nullptr;
+  }
+}
+template <bool PD>
+KernelFn pick_pair(int S, int RI, int VI) {
+  constexpr int R0 = rows_fwd(3, 0), R1 = rows_fwd(3, 1);
+  if (S == 1) return RI == 0 ? pick_pair_v<1, R0, PD>(VI) : pick_pair_v<1, R1, PD>(VI);
+  return RI == 0 ? pick_pair_v<2, R0, PD>(VI) : pick_pair_v<2, R1, PD>(VI);
+}
+
+KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair) {
+  if (pair) {
+    if (dtype != DWCONV_BF16 || K != 3) return nullptr;
+    return padded ? pick_pair<true>(S, RI, VI) : pick_pair<false>(S, RI, VI);
+  }
   if (dtype == DWCONV_F32) return padded ? pick_t<float, true>(K, S, RI, VI) : pick_t<float, false>(K, S, RI, VI);
   return padded ? pick_t<__nv_bfloat16, true>(K, S, RI, VI) : pick_t<__nv_bfloat16, false>(K, S, RI, VI);
 }

@@ -85,8 +85,8 @@ int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb, int K) {
   return 0;
 }
 
-KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded) {
-  if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI, padded);
+KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false) {
+  if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI, padded, pair);
   if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded);
   if (pass == kPassBwdFused) return bwd_fused_kernel(dtype, K, S, RI, VI, padded);
   return bwd_filter_kernel(dtype, K, S, RI, VI, padded);
@@ -282,7 +282,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, nst);
       if (c.smem_bytes > max_smem_optin) layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, 2);
       if (c.smem_bytes > max_smem_optin) return;
-      KernelFn kf = kernel_for(pass, g.dtype, K, S, c.ri, c.vi, c.padded);
+      KernelFn kf = kernel_for(pass, g.dtype, K, S, c.ri, c.vi, c.padded, c.pair);
       const int ctas = kf ? occupancy(kf, c.smem_bytes, c.threads) : 0;  // resident CTAs per SM
       if (ctas < 1) return;
       const int64_t grid = std::min<int64_t>(nch, (int64_t)ctas * num_sms);
@@ -305,7 +305,12 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       for (int T : kT) {
         for (int64_t P = al; P <= std::max<int64_t>(pmax, al); P += al) {
           if (P > Q) break;
-          const int64_t tiles = P * tpp;
+          // bf16 fwd, whole planes, m = 1: plane-pair strips (half the tiles, each twice the work)
+          static const bool pair_env = env_int("DWCONV_BF16_PAIR", 1, 0, 1) == 1;
+          p->pair = pair_env && fwd && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
+                    ((S * p->V) % 2 == 0) && kernel_for(pass, g.dtype, K, S, p->ri, p->vi, pad_full, true) != nullptr;
+          const int64_t tiles = p->pair ? (P + 1) / 2 * tpp : P * tpp;
+          const int64_t useful = p->pair ? (Q + 1) / 2 * tpp : Q * tpp;
           const int64_t nch = (Q + P - 1) / P;
           int64_t inb = P * in_plane;
           if (pad_full)  // zero rows above each plane, below the last, and strip overrun
@@ -313,7 +318,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
           p->padded = pad_full;
           p->zbe = (int)(zbe_b / eb);
           p->pitch = (int)((zbe_b + round16(Hin * Win * eb)) / eb);
-          consider(T, (int)P, 1, out_rows_total, tiles, nch, Q * tpp, inb, P * out_plane, 2 * P * wpp);
+          consider(T, (int)P, 1, out_rows_total, tiles, nch, useful, inb, P * out_plane, 2 * P * wpp);
         }
       }
     }
@@ -325,6 +330,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
         if (inb + outb > budget_max) break;
         const int nb = (nsb_full + nsb_b - 1) / nsb_b;
         for (int T : kT) {
+          p->pair = false;
           const int64_t tiles = (int64_t)nsb_b * p->ncg;
           if (pad_band) {
             const int64_t rows_buf = (fwd ? (int64_t)(br - 1) * S + K : (br + K - 1 + S - 1) / S + 1) + PADr;
@@ -345,7 +351,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     p->nchunks = (p->nbands == 1) ? (Q + p->P - 1) / p->P : Q * p->nbands;
     if (p->nchunks >= ((int64_t)1 << 31)) return false;
     p->nsb = (p->band_rows + R - 1) / R;
-    KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded);
+    KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded, p->pair);
     if (!fn) return false;
     const int occ = occupancy(fn, p->smem_bytes, p->threads);
     if (occ < 1) return false;
@@ -504,6 +510,8 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   a.div_c = make_fastdiv((uint32_t)g.C);
   static const int dbg = nchw::env_int("DWCONV_DEBUG", 0, 0, 3);
   a.dbg = dbg;
+  static const int early = nchw::env_int("DWCONV_EARLY_PDL", 1, 0, 1);
+  a.early_pdl = early;
   a.div_nb = make_fastdiv((uint32_t)std::max(1, p.nbands));
   return a;
 }
@@ -513,7 +521,7 @@ cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, co
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.w = w; a.out = y;
   a.wbulk = weights_bulk_ok(g, w);
-  nchw::KernelFn fn = nchw::fwd_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  nchw::KernelFn fn = nchw::fwd_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded, p.pair);
   return launch(fn, p, st, a);
 }
 

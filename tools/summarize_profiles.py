@@ -1,8 +1,9 @@
 """Summarise ncu captures (from tools/profile_round.sh) into profiles/<round>/.
 
-* launch list: the last 39 dwconv launches of the bench run are the per-kernel
-  timing pass, in bench step order (13 fwd, then bwd_data/bwd_filter per layer in
-  reverse).  Writes a markdown table and profiles/ncu_traffic.json (DRAM bytes
+* launch list: the last 39 dwconv launches of the bench run (``--kernel-reps 0``)
+  are its last timed step, in step order (13 fwd, then bwd_data/bwd_filter per
+  layer in reverse; the two backward kernels of a layer may appear in either
+  order because bwd_filter runs on a side stream).  Writes a markdown table and profiles/ncu_traffic.json (DRAM bytes
   read+write per launch, keyed like bench.py's roofline lookup).
 * full reports: key metrics of each ``full_<layer>_<pass>.ncu-rep``.
 
