@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
       stage_coop<T>(sx, x_src(r), xs);
       stage_coop<T>(sdy, dy_src(r), dy_spec(r));
     }
-    if (PADDED && a.nbands > 1 && r.hi == H) zero_elems(sx + xs.zbe + xs.cnt, PAD * W);  // rows under the last band
+    if (PADDED && a.nbands > 1 && r.hi == H)  // rows under the last band of every plane
+      for (int pl = 0; pl < np; ++pl) zero_elems(sx + pl * xs.pitch + xs.zbe + xs.cnt, PAD * W);
     __syncthreads();
     if (active) {
       const int rows_x = r.hi - r.lo;

@@ -134,7 +134,7 @@ int est_ctas_per_sm(int smem_bytes, int threads) {
 // work, discounted when chunks are tiny (per-chunk fixed costs) or the SM holds
 // too few warps to hide shared-memory latency.
 double chunk_score(int64_t useful, int64_t slots, int64_t chunk_bytes, int smem, int threads) {
-  static const double min_chunk = 1024.0 * nchw::env_int("DWCONV_MIN_CHUNK_KB", 16, 1, 64);
+  static const double min_chunk = 1024.0 * nchw::env_int("DWCONV_MIN_CHUNK_KB", 32, 1, 64);
   static const double occ_warps = nchw::env_int("DWCONV_OCC_WARPS", 16, 4, 64);
   const double eff = (double)useful / (double)slots;
   const double size_f = std::min(1.0, std::sqrt((double)chunk_bytes / min_chunk));
@@ -377,7 +377,15 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   const int64_t zbe_b = round16(PADr * g.W * eb);
   const bool pad_full = (g.H * g.W * eb) % 16 == 0;
   const bool pad_band = (g.W * eb) % 16 == 0;
+  // tuning aid: DWCONV_BF_FORCE="P,tpg,nsb" pins the chunk shape (nsb = strip rows per band, 0 = whole planes)
+  static const int* bf_force = []() -> const int* {
+    static int f[3];
+    const char* e = getenv("DWCONV_BF_FORCE");
+    if (!e || sscanf(e, "%d,%d,%d", &f[0], &f[1], &f[2]) != 3) return nullptr;
+    return f;
+  }();
   auto consider = [&](int P, int tpg, int nb, int br, int64_t xb, int64_t dyb) {
+    if (bf_force && (P != bf_force[0] || tpg != bf_force[1] || (nb == 1 ? 0 : (br + R - 1) / R) != bf_force[2])) return;
     if (nb == 1 ? pad_full : pad_band) {  // padded x staging
       const int64_t rows_buf = (nb == 1) ? g.H : (int64_t)(br - 1) * S + K + PADr;
       const int64_t pitch_b = zbe_b + round16(rows_buf * g.W * eb);
@@ -427,7 +435,8 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       const int64_t dyb = (int64_t)m * std::min<int64_t>(g.Ho, br + (fused ? 2 * PADr : 0)) * g.Wo * eb;
       if (xb + dyb > budget_max) break;
       const int nb = (nsb_full + nsb_b - 1) / nsb_b;
-      for (int tpg = 1; m * tpg <= kThreads; ++tpg) consider(1, tpg, nb, br, xb, dyb);
+      for (int P = 1; P * m <= kThreads && P <= g.C && P * (xb + dyb) <= budget_max; ++P)  // P planes per band chunk
+        for (int tpg = 1; P * m * tpg <= kThreads; ++tpg) consider(P, tpg, nb, br, P * xb, P * dyb);
     }
   }
   if (best < 0.0) return false;

@@ -78,8 +78,22 @@ def main():
     layers = synth.mobilenet_v1_dw(a.batch, a.alpha, a.res)
     step = [("fwd", L) for L in layers] + [(p, L) for L in reversed(layers) for p in ("bwd_data", "bwd_filter")]
 
-    launches = [l for l in read_launches(os.path.join(a.src, "launches.csv")) if "nchw_" in l["name"] or "generic_" in l["name"]]
-    last = launches[-len(step):]
+    launches = [l for l in read_launches(os.path.join(a.src, "launches.csv"))
+                if any(t in l["name"] for t in ("nchw_", "generic_", "dbf_kernel", "nhwc_"))]
+
+    def kind(name):
+        if "fwd_kernel" in name or "generic_fwd" in name:
+            return "fwd"
+        if "bwd_data" in name:
+            return "bwd_data"
+        return "bwd_filter"
+    # the streams interleave under ncu's serialisation: take the last 13 launches of each
+    # pass; within a pass the order is fixed (fwd: layer order, backward: reverse order)
+    per = {k: [l for l in launches if kind(l["name"]) == k][-len(layers):] for k in ("fwd", "bwd_data", "bwd_filter")}
+    last = []
+    for (pas, L) in step:
+        idx = [i for i, (p2, _) in enumerate(step) if p2 == pas].index(step.index((pas, L)))
+        last.append(per[pas][idx])
     tot = sum(l["gpu__time_duration.sum"] for l in last)
     md = ["# ncu launch list — one bench step (per-kernel timing pass, serialised, cold-ish cache)", "",
           f"workload: MobileNet-v1 a{a.alpha:g} r{a.res} batch {a.batch} {a.dtype} {a.layout}; "
