@@ -37,7 +37,9 @@ __device__ __forceinline__ ChunkRows bd_rows(const NArgs& a, int64_t c) {
   return k;
 }
 
-template <class T, int K, int S, int R, int V, bool PADDED>
+// PAIR (bf16, S = 1, m = 1): strips of two dx planes at once through
+// stencil_strip_pair (FFMA2 lanes = planes), flipped kernels.
+template <class T, int K, int S, int R, int V, bool PADDED, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int D0 = floor_div(PAD - K + 1, S);
@@ -134,7 +136,51 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
       const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
       const T* swr = reinterpret_cast<const T*>(swc) + ww.off;  // raw rows (ww.tma), flipped on read for S == 1
       const int rows_dy = k.hi - k.lo;
-      const int ntiles = k.np * a.nsb * ncg;
+      if constexpr (PAIR) {  // m == 1: dy plane pp feeds dx plane pp
+        const int npair = (k.np + 1) >> 1;
+        const int ntp = npair * a.nsb * ncg;
+        for (int t = ctid; t < ntp; t += nct) {
+          const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
+          const int cb = t - t2 * ncg;
+          const int pp2 = (int)fdiv((uint32_t)t2, a.div_nsb);
+          const int sb = t2 - pp2 * a.nsb;
+          const int ppa = 2 * pp2;
+          const bool hasb = ppa + 1 < k.np;
+          const int ppb = hasb ? ppa + 1 : ppa;
+          const int ih0 = k.r0 + sb * R;
+          const int iw0 = cb * V;
+          float2 wp[KK];
+          if (ww.tma) {
+#pragma unroll
+            for (int q = 0; q < KK; ++q)
+              wp[q] = make_float2(Elem<T>::load(swr + ppa * KK + KK - 1 - q), Elem<T>::load(swr + ppb * KK + KK - 1 - q));
+          } else {
+#pragma unroll
+            for (int q = 0; q < KK; ++q) wp[q] = make_float2(swc[ppa * KK + q], swc[ppb * KK + q]);
+          }
+          float2 acc[R][V];
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+            for (int u = 0; u < V; ++u) acc[tt][u] = make_float2(0.f, 0.f);
+          const T* base = sin + sp.zbe - k.lo * Wo;
+          stencil_strip_pair<K, 1, R, V, PADDED>(base + ppa * sp.pitch, base + ppb * sp.pitch, zrow, Wo, k.lo, rows_dy,
+                                                 ih0 - PAD, iw0, wp, acc);
+          T* xa = dx + (k.q0 + ppa) * (int64_t)H * W + iw0;
+          T* xb = xa + (int64_t)H * W;
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt) {
+            if (ih0 + tt < k.r1) {
+              float va[V], vb[V];
+#pragma unroll
+              for (int u = 0; u < V; ++u) { va[u] = acc[tt][u].x; vb[u] = acc[tt][u].y; }
+              VecIO<T, V>::store(xa + (int64_t)(ih0 + tt) * W, va);
+              if (hasb) VecIO<T, V>::store(xb + (int64_t)(ih0 + tt) * W, vb);
+            }
+          }
+        }
+      }
+      const int ntiles = PAIR ? 0 : k.np * a.nsb * ncg;
       for (int t = ctid; t < ntiles; t += nct) {
         const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
         const int cb = t - t2 * ncg;
@@ -278,7 +324,25 @@ KernelFn pick_t(int K, int S, int RI, int VI) {
 
 }  // namespace
 
-KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded) {
+// bf16 plane-pair kernels (S = 1, 3x3): V even.
+template <int R, bool PD>
+KernelFn pick_pair_v(int VI) {
+  using B = __nv_bfloat16;
+  switch (VI) {
+    case 1: return nchw_bwd_data_kernel<B, 3, 1, R, 2, PD, true>;
+    case 2: if constexpr (PD) return nchw_bwd_data_kernel<B, 3, 1, R, 4, PD, true>; else return nullptr;
+    case 3: if constexpr (PD) return nchw_bwd_data_kernel<B, 3, 1, R, 8, PD, true>; else return nullptr;
+    default: return nullptr;
+  }
+}
+
+KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair) {
+  if (pair) {
+    if (dtype != DWCONV_BF16 || K != 3 || S != 1) return nullptr;
+    constexpr int R0 = rows_bd(3, 1, 0), R1 = rows_bd(3, 1, 1);
+    if (RI == 0) return padded ? pick_pair_v<R0, true>(VI) : pick_pair_v<R0, false>(VI);
+    return padded ? pick_pair_v<R1, true>(VI) : pick_pair_v<R1, false>(VI);
+  }
   if (dtype == DWCONV_F32) return padded ? pick_t<float, true>(K, S, RI, VI) : pick_t<float, false>(K, S, RI, VI);
   return padded ? pick_t<__nv_bfloat16, true>(K, S, RI, VI) : pick_t<__nv_bfloat16, false>(K, S, RI, VI);
 }

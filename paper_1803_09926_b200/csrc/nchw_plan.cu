@@ -87,7 +87,7 @@ int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb, int K) {
 
 KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false) {
   if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI, padded, pair);
-  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded);
+  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded, pair);
   if (pass == kPassBwdFused) return bwd_fused_kernel(dtype, K, S, RI, VI, padded);
   return bwd_filter_kernel(dtype, K, S, RI, VI, padded);
 }
@@ -307,7 +307,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
           if (P > Q) break;
           // bf16 fwd, whole planes, m = 1: plane-pair strips (half the tiles, each twice the work)
           static const bool pair_env = env_int("DWCONV_BF16_PAIR", 1, 0, 1) == 1;
-          p->pair = pair_env && fwd && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
+          p->pair = pair_env && (fwd || S == 1) && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
                     ((S * p->V) % 2 == 0) && kernel_for(pass, g.dtype, K, S, p->ri, p->vi, pad_full, true) != nullptr;
           const int64_t tiles = p->pair ? (P + 1) / 2 * tpp : P * tpp;
           const int64_t useful = p->pair ? (Q + 1) / 2 * tpp : Q * tpp;
@@ -539,7 +539,7 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
   nchw::NArgs a = base_args(g, p);
   a.in = dy; a.w = w; a.out = dx;
   a.wbulk = weights_bulk_ok(g, w);
-  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
+  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded, p.pair);
   return launch(fn, p, st, a);
 }
 
