@@ -37,17 +37,16 @@ __device__ __forceinline__ ChunkRows bd_rows(const NArgs& a, int64_t c) {
   return k;
 }
 
-// PAIR (bf16, S = 1, m = 1): strips of two dx planes at once through
-// stencil_strip_pair (FFMA2 lanes = planes), flipped kernels.
+// PAIR (bf16, m = 1): tiles of two dx planes at once, FFMA2 lanes = planes --
+// S = 1 through stencil_strip_pair (flipped kernels), S = 2 polyphase.
 template <class T, int K, int S, int R, int V, bool PADDED, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int D0 = floor_div(PAD - K + 1, S);
   constexpr int NRY = floor_div(R - 1 + PAD, S) - D0 + 1;
-  constexpr int NCY = floor_div(S - 1 + PAD, S) - D0 + 1;
-  constexpr int TW = (S == 1) ? V : S;  // dx columns per thread tile
+  constexpr int TW = (S == 1) ? V : S * V;  // dx columns per thread tile (stride aligned)
+  constexpr int NCY = floor_div(TW - 1 + PAD, S) - D0 + 1;
   static_assert(R % S == 0, "dx strip must be stride aligned");
-  static_assert(S == 1 || V == 1, "stride-2 tiles are scalar");
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 64);
@@ -148,34 +147,84 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
           const bool hasb = ppa + 1 < k.np;
           const int ppb = hasb ? ppa + 1 : ppa;
           const int ih0 = k.r0 + sb * R;
-          const int iw0 = cb * V;
+          const int iw0 = cb * TW;
           float2 wp[KK];
           if (ww.tma) {
 #pragma unroll
-            for (int q = 0; q < KK; ++q)
-              wp[q] = make_float2(Elem<T>::load(swr + ppa * KK + KK - 1 - q), Elem<T>::load(swr + ppb * KK + KK - 1 - q));
+            for (int q = 0; q < KK; ++q) {
+              const int qq = (S == 1) ? (KK - 1 - q) : q;
+              wp[q] = make_float2(Elem<T>::load(swr + ppa * KK + qq), Elem<T>::load(swr + ppb * KK + qq));
+            }
           } else {
 #pragma unroll
             for (int q = 0; q < KK; ++q) wp[q] = make_float2(swc[ppa * KK + q], swc[ppb * KK + q]);
           }
-          float2 acc[R][V];
+          float2 acc[R][TW];
 #pragma unroll
           for (int tt = 0; tt < R; ++tt)
 #pragma unroll
-            for (int u = 0; u < V; ++u) acc[tt][u] = make_float2(0.f, 0.f);
+            for (int u = 0; u < TW; ++u) acc[tt][u] = make_float2(0.f, 0.f);
           const T* base = sin + sp.zbe - k.lo * Wo;
-          stencil_strip_pair<K, 1, R, V, PADDED>(base + ppa * sp.pitch, base + ppb * sp.pitch, zrow, Wo, k.lo, rows_dy,
-                                                 ih0 - PAD, iw0, wp, acc);
+          if constexpr (S == 1) {
+            stencil_strip_pair<K, 1, R, V, PADDED>(base + ppa * sp.pitch, base + ppb * sp.pitch, zrow, Wo, k.lo,
+                                                   rows_dy, ih0 - PAD, iw0, wp, acc);
+          } else {  // polyphase, as in the scalar path below, with (plane A, plane B) lanes
+            const int ohb = ih0 / S + D0;
+            const int owb = iw0 / S + D0;
+            bool cok[NCY];
+#pragma unroll
+            for (int cy = 0; cy < NCY; ++cy) cok[cy] = (unsigned)(owb + cy) < (unsigned)Wo;
+            const T* spa = base + ppa * sp.pitch + owb;
+            const T* spb = base + ppb * sp.pitch + owb;
+#pragma unroll
+            for (int ry = 0; ry < NRY; ++ry) {
+              const int oh = ohb + ry;
+              const bool rok = PADDED || (unsigned)(oh - k.lo) < (unsigned)rows_dy;
+              const T* pa = rok ? spa + oh * Wo : zrow + owb;
+              const T* pb = rok ? spb + oh * Wo : zrow + owb;
+              float2 v[NCY];
+#pragma unroll
+              for (int cy = 0; cy < NCY; ++cy)
+                v[cy] = cok[cy] ? make_float2(Elem<T>::load(pa + cy), Elem<T>::load(pb + cy)) : make_float2(0.f, 0.f);
+#pragma unroll
+              for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                  const int th = tt + PAD - i;
+                  if (pmod(th, S) == 0 && floor_div(th, S) - D0 == ry) {
+#pragma unroll
+                    for (int u = 0; u < TW; ++u)
+#pragma unroll
+                      for (int jj = 0; jj < K; ++jj) {
+                        const int tw = u + PAD - jj;
+                        if (pmod(tw, S) == 0) {
+                          const int cy = floor_div(tw, S) - D0;
+                          acc[tt][u] = __ffma2_rn(wp[i * K + jj], v[cy], acc[tt][u]);
+                        }
+                      }
+                  }
+                }
+            }
+          }
           T* xa = dx + (k.q0 + ppa) * (int64_t)H * W + iw0;
           T* xb = xa + (int64_t)H * W;
 #pragma unroll
           for (int tt = 0; tt < R; ++tt) {
             if (ih0 + tt < k.r1) {
-              float va[V], vb[V];
+              float va[TW], vb[TW];
 #pragma unroll
-              for (int u = 0; u < V; ++u) { va[u] = acc[tt][u].x; vb[u] = acc[tt][u].y; }
-              VecIO<T, V>::store(xa + (int64_t)(ih0 + tt) * W, va);
-              if (hasb) VecIO<T, V>::store(xb + (int64_t)(ih0 + tt) * W, vb);
+              for (int u = 0; u < TW; ++u) { va[u] = acc[tt][u].x; vb[u] = acc[tt][u].y; }
+              if (S == 1 || W % TW == 0) {
+                VecIO<T, TW>::store(xa + (int64_t)(ih0 + tt) * W, va);
+                if (hasb) VecIO<T, TW>::store(xb + (int64_t)(ih0 + tt) * W, vb);
+              } else {
+#pragma unroll
+                for (int u = 0; u < TW; ++u)
+                  if (iw0 + u < W) {
+                    Elem<T>::store(xa + (int64_t)(ih0 + tt) * W + u, va[u]);
+                    if (hasb) Elem<T>::store(xb + (int64_t)(ih0 + tt) * W + u, vb[u]);
+                  }
+              }
             }
           }
         }
@@ -216,7 +265,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
                                                  part);
           } else {
             const int ohb = ih0 / S + D0;
-            const int owb = cb + D0;
+            const int owb = iw0 / S + D0;
             bool cok[NCY];
 #pragma unroll
             for (int cy = 0; cy < NCY; ++cy) cok[cy] = (unsigned)(owb + cy) < (unsigned)Wo;
@@ -237,7 +286,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
                   const int th = tt + PAD - i;  // relative to ih0
                   if (pmod(th, S) == 0 && floor_div(th, S) - D0 == ry) {
 #pragma unroll
-                    for (int u = 0; u < S; ++u)
+                    for (int u = 0; u < TW; ++u)
 #pragma unroll
                       for (int jj = 0; jj < K; ++jj) {
                         const int tw = u + PAD - jj;
@@ -261,16 +310,16 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
           for (int tt = 0; tt < R; ++tt)
             if (ih0 + tt < k.r1) VecIO<T, V>::store(xo + (int64_t)(ih0 + tt) * W, acc[tt]);
         } else {
-          const bool pair = (W % 2 == 0);  // stride-aligned column pair fits and is 2-element aligned
+          const bool whole = (W % TW == 0);  // the tile's columns fit and are TW-element aligned
 #pragma unroll
           for (int tt = 0; tt < R; ++tt) {
             if (ih0 + tt >= k.r1) continue;
             T* row = xo + (int64_t)(ih0 + tt) * W;
-            if (S == 2 && pair) {
-              VecIO<T, 2>::store(row, acc[tt]);
+            if (whole) {
+              VecIO<T, TW>::store(row, acc[tt]);
             } else {
 #pragma unroll
-              for (int u = 0; u < S; ++u)
+              for (int u = 0; u < TW; ++u)
                 if (iw0 + u < W) Elem<T>::store(row + u, acc[tt][u]);
             }
           }
@@ -305,9 +354,15 @@ KernelFn pick_rv(int RI, int VI) {
   }
     if (RI == 0) { DW_V(R0) } else { DW_V(R1) }
 #undef DW_V
-  } else {
-    if (VI != 0) return nullptr;
-    return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 1, PD> : nchw_bwd_data_kernel<T, K, S, R1, 1, PD>;
+  } else {  // stride 2: tiles of R rows x 2V columns
+    switch (VI) {
+      case 0: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 1, PD> : nchw_bwd_data_kernel<T, K, S, R1, 1, PD>;
+      case 1: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 2, PD> : nchw_bwd_data_kernel<T, K, S, R1, 2, PD>;
+      case 2:
+        if constexpr (K == 3) return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 4, PD> : nchw_bwd_data_kernel<T, K, S, R1, 4, PD>;
+        else return nullptr;
+      default: return nullptr;
+    }
   }
 }
 
@@ -338,7 +393,20 @@ KernelFn pick_pair_v(int VI) {
 
 KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair) {
   if (pair) {
-    if (dtype != DWCONV_BF16 || K != 3 || S != 1) return nullptr;
+    if (dtype != DWCONV_BF16 || K != 3) return nullptr;
+    if (S == 2) {  // polyphase pair tiles, 2V columns
+      using B = __nv_bfloat16;
+      constexpr int R0 = rows_bd(3, 2, 0), R1 = rows_bd(3, 2, 1);
+      switch (VI) {
+        case 0: return RI == 0 ? (padded ? nchw_bwd_data_kernel<B, 3, 2, R0, 1, true, true> : nchw_bwd_data_kernel<B, 3, 2, R0, 1, false, true>)
+                               : (padded ? nchw_bwd_data_kernel<B, 3, 2, R1, 1, true, true> : nchw_bwd_data_kernel<B, 3, 2, R1, 1, false, true>);
+        case 1: return RI == 0 ? (padded ? nchw_bwd_data_kernel<B, 3, 2, R0, 2, true, true> : nchw_bwd_data_kernel<B, 3, 2, R0, 2, false, true>)
+                               : (padded ? nchw_bwd_data_kernel<B, 3, 2, R1, 2, true, true> : nchw_bwd_data_kernel<B, 3, 2, R1, 2, false, true>);
+        case 2: return RI == 0 ? (padded ? nchw_bwd_data_kernel<B, 3, 2, R0, 4, true, true> : nchw_bwd_data_kernel<B, 3, 2, R0, 4, false, true>)
+                               : (padded ? nchw_bwd_data_kernel<B, 3, 2, R1, 4, true, true> : nchw_bwd_data_kernel<B, 3, 2, R1, 4, false, true>);
+        default: return nullptr;
+      }
+    }
     constexpr int R0 = rows_bd(3, 1, 0), R1 = rows_bd(3, 1, 1);
     if (RI == 0) return padded ? pick_pair_v<R0, true>(VI) : pick_pair_v<R0, false>(VI);
     return padded ? pick_pair_v<R1, true>(VI) : pick_pair_v<R1, false>(VI);

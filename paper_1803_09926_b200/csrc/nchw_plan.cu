@@ -241,9 +241,17 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     p->ri = (out_rows_total % rows_for(pass, K, S, 0) == 0) ? 0 : 1;
     p->R = rows_for(pass, K, S, p->ri);
     if (fwd) p->vi = pick_vi(g.Wo, g.W, S, eb, K);
-    else p->vi = (S == 1) ? pick_vi(g.W, g.Wo, 1, eb, K) : 0;
+    else if (S == 1) p->vi = pick_vi(g.W, g.Wo, 1, eb, K);
+    else {  // stride-2 dx tiles of 2V columns: rows must split into whole, aligned tiles
+      p->vi = 0;
+      static const int wide = env_int("DWCONV_BD_WIDE", 1, 0, 2);  // 1: 4-column tiles (measured best)
+      for (int vi = std::min(wide, K == 3 ? 2 : 1); vi > 0; --vi) {
+        const int64_t tw = (int64_t)S << vi;
+        if (g.W % tw == 0 && (g.W * eb) % std::min<int64_t>(16, tw * eb) == 0) { p->vi = vi; break; }
+      }
+    }
     p->V = 1 << p->vi;
-    p->ncg = fwd ? (int)(g.Wo / p->V) : (S == 1 ? (int)(g.W / p->V) : (int)((g.W + S - 1) / S));
+    p->ncg = fwd ? (int)(g.Wo / p->V) : (S == 1 ? (int)(g.W / p->V) : (int)((g.W + S * p->V - 1) / (S * p->V)));
     const int R = p->R;
     const int nsb_full = (out_rows_total + R - 1) / R;
     const int64_t tpp = (int64_t)nsb_full * p->ncg;  // thread strips per plane
@@ -307,7 +315,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
           if (P > Q) break;
           // bf16 fwd, whole planes, m = 1: plane-pair strips (half the tiles, each twice the work)
           static const bool pair_env = env_int("DWCONV_BF16_PAIR", 1, 0, 1) == 1;
-          p->pair = pair_env && (fwd || S == 1) && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
+          p->pair = pair_env && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
                     ((S * p->V) % 2 == 0) && kernel_for(pass, g.dtype, K, S, p->ri, p->vi, pad_full, true) != nullptr;
           const int64_t tiles = p->pair ? (P + 1) / 2 * tpp : P * tpp;
           const int64_t useful = p->pair ? (Q + 1) / 2 * tpp : Q * tpp;
