@@ -44,6 +44,12 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   const int64_t n1 = min(a.N, n0 + a.nps);
   const int iters = (int)(n1 - n0) * a.nbands;
 
+  // empty[st]: every warp arrives after computing on stage st; thread 0 waits on it
+  // before refilling st, so warps never wait for each other inside the loop
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 72);  // <= 7 stages below the zero row at 128
+  const int nwarps = (int)(blockDim.x >> 5);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < a.ns; ++i) mbar_init(&empty[i], nwarps);
   prologue(smem, bars, a);
   auto sx_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
   auto sdy_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + a.in2_off + st * a.in_stage); };
@@ -120,20 +126,29 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   int st = 0;
   uint32_t par = 0;
   for (int kk = 0; kk < iters; ++kk) {
-    if (threadIdx.x == 0 && kk + a.ns - 1 < iters) issue(kk + a.ns - 1, st == 0 ? a.ns - 1 : st - 1);
+    if (threadIdx.x == 0 && kk + a.ns - 1 < iters) {
+      const int rs = (st == 0) ? a.ns - 1 : st - 1;  // the stage consumed in iteration kk - 1
+      if (kk >= 1) mbar_wait(&empty[rs], (uint32_t)(((kk - 1) / a.ns) & 1));
+      issue(kk + a.ns - 1, rs);
+    }
     const Rows r = rows_of(kk);
+    const int cur = st;
     T* sx = sx_of(st);
     T* sdy = sdy_of(st);
     mbar_wait(&bars[st], par);
     if (++st == a.ns) { st = 0; par ^= 1; }
     const StageSpec xs = x_spec(r);
-    if (!chunk_bulk(r)) {
-      stage_coop<T>(sx, x_src(r), xs);
-      stage_coop<T>(sdy, dy_src(r), dy_spec(r));
+    const bool bulk = chunk_bulk(r);
+    const bool zbot = PADDED && a.nbands > 1 && r.hi == H;
+    if (!bulk || zbot) {  // uniform over the CTA
+      if (!bulk) {
+        stage_coop<T>(sx, x_src(r), xs);
+        stage_coop<T>(sdy, dy_src(r), dy_spec(r));
+      }
+      if (zbot)  // rows under the last band of every plane
+        for (int pl = 0; pl < np; ++pl) zero_elems(sx + pl * xs.pitch + xs.zbe + xs.cnt, PAD * W);
+      __syncthreads();
     }
-    if (PADDED && a.nbands > 1 && r.hi == H)  // rows under the last band of every plane
-      for (int pl = 0; pl < np; ++pl) zero_elems(sx + pl * xs.pitch + xs.zbe + xs.cnt, PAD * W);
-    __syncthreads();
     if (active) {
       const int rows_x = r.hi - r.lo;
       const int rows_dy = r.dhi - r.dlo;
@@ -209,8 +224,10 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
 #pragma unroll
       for (int q = 0; q < KK; ++q) run[q] += kPacked ? (loc2[q].x + loc2[q].y) : loc[q];
     }
-    __syncthreads();  // the stage just consumed is refilled by the next issue
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[cur]);  // this warp is done with the stage
   }
+  __syncthreads();  // all warps are done with the stages before the sums are parked in them
 
   griddep_launch_dependents();
   // ---- reduce over the tpg threads of each dy plane: every thread parks its sums

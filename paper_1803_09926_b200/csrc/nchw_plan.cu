@@ -36,7 +36,7 @@ int chunk_budget() {  // target bytes of one chunk (input + output)
 }
 
 int num_stages() {
-  static int ns = env_int("DWCONV_STAGES", 2, 2, 8);
+  static int ns = env_int("DWCONV_STAGES", 2, 2, 7);  // bwd_filter keeps 7 empty barriers at smem[72..128)
   return ns;
 }
 
