@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--fused", default="none", choices=["none", "all", "small"],
                     help="layers whose backward uses the fused dwconv_bwd (one pass over x and dy) instead of "
                          "bwd_data + bwd_filter on two streams: none, all fusable, or the fusable 14x14/7x7 layers")
+    ap.add_argument("--no-tune", action="store_true", help="keep the planner's launch shapes (no measured selection)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -248,6 +249,15 @@ def main():
                  dw=bucket.views[len(bufs)],
                  wsb=ops.dwconv_bwd_filter_workspace_bytes(d))
         bufs.append(b)
+    # measured plan selection (tune.py): time every candidate launch shape of each
+    # pass on this layer's tensors and keep the fastest (before any graph capture)
+    tuned = {}
+    if not args.no_tune:
+        from paper_1803_09926_b200 import tune
+        for b in bufs:
+            tuned[b["L"].name] = tune.tune_layer(b["d"], b["x"], b["dy"], b["w"])
+            b["wsb"] = ops.dwconv_bwd_filter_workspace_bytes(b["d"])
+        torch.cuda.synchronize()
     ws = torch.zeros(max(16, max(b["wsb"] for b in bufs)), dtype=torch.uint8, device=dev)
     footprint = sum(b[k].numel() * b[k].element_size() for b in bufs for k in ("x", "w", "dy", "y", "dx"))
 
@@ -484,7 +494,11 @@ def main():
                        "l2": f"no flush: step footprint {footprint / 1e9:.2f} GB >> 126 MB L2",
                        "graph": graph is not None,
                        "schedule": ("serial" if args.serial else "bwd_filter on a side stream (overlaps bwd_data)") +
-                                   f"; fused backward on {sum(b['fused'] for b in bufs)}/13 layers"},
+                                   f"; fused backward on {sum(b['fused'] for b in bufs)}/13 layers",
+                       "plans": ("planner defaults" if not tuned else
+                                 "measured selection (tune.py, before the timed region): "
+                                 f"{sum(1 for t in tuned.values() for v in t.values() if v['index'] != 0)} of "
+                                 f"{sum(len(t) for t in tuned.values())} tuned passes changed")},
             "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / world / peak,
             "algorithmic_bytes_per_step": sbytes * world,
             "roofline": ({"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
@@ -500,6 +514,7 @@ def main():
             "paper_context": {"img_s": PAPER_CONTEXT_IMG_S, "hw": "GTX 1080 Ti, Caffe, Table III (context only)"},
         }
         if args.extra:
+            line["tuning"] = tuned
             line["kernels"] = [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in kk.items()} for kk in kt]
         print(json.dumps(line), flush=True)
     if world > 1:

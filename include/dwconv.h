@@ -171,6 +171,28 @@ typedef struct {
 } dwconv_plan_info;
 DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info);
 
+/* Measurement-driven plan selection (cf. a "find" step): the NCHW chunk family's
+ * distinct launch shapes for (d, pass), the planner's default first, then by the
+ * planner's score.  The caller times them on its own buffers and installs the
+ * fastest with dwconv_plan_select; later calls with the same descriptor and pass
+ * on the same device use it.  Selection changes only the launch shape (chunking,
+ * CTA size, batch slices), never the arithmetic contract: every candidate meets
+ * the parity rules of DESIGN.md §5, and a bwd_filter candidate may need a
+ * different workspace size (dwconv_bwd_filter_workspace_bytes reflects the
+ * selection; re-query after selecting, and zero-fill a new workspace).
+ *   dwconv_plan_candidates: pass in {FWD, BWD_DATA, BWD_FILTER}; writes at most
+ *     max_candidates entries to infos (caller-owned array) and the number written
+ *     to *count; max_candidates = 0 only reports the total in *count.  Non-NCHW
+ *     layouts, N = 0 and the generic override report 0 candidates.
+ *   dwconv_plan_select: index into the same list; -1 restores the planner's pick.
+ *     Returns DWCONV_ERR_BAD_DESCRIPTOR if the list was not queried first or the
+ *     index is out of range.  Both are host-only calls (no launches) and
+ *     thread-safe; neither may be called during stream capture of the same pass. */
+#define DWCONV_MAX_CANDIDATES 24
+DWCONV_API int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, dwconv_plan_info* infos,
+                                      int* count);
+DWCONV_API int dwconv_plan_select(const dwconv_desc* d, int pass, int index);
+
 /* Force a kernel family for testing: 0 = automatic (default), 1 = generic only. */
 DWCONV_API int dwconv_set_variant_override(int variant);
 

@@ -18,7 +18,9 @@ VARIANTS = {0: "none", 1: "generic", 2: "nchw_chunk", 3: "nhwc_tile"}
 FUNCTIONS = ("dwconv_abi_version", "dwconv_status_string", "dwconv_output_shape", "dwconv_fwd",
              "dwconv_bwd_data", "dwconv_bwd_filter_workspace_bytes", "dwconv_bwd_filter",
              "dwconv_bwd_workspace_bytes", "dwconv_bwd",
-             "dwconv_workspace_init", "dwconv_plan", "dwconv_set_variant_override")
+             "dwconv_workspace_init", "dwconv_plan", "dwconv_plan_candidates", "dwconv_plan_select",
+             "dwconv_set_variant_override")
+MAX_CANDIDATES = 24
 
 
 class Desc(ctypes.Structure):
@@ -70,9 +72,12 @@ def load() -> ctypes.CDLL:
     lib.dwconv_bwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.dwconv_workspace_init.argtypes = [vp, sz, vp]
     lib.dwconv_plan.argtypes = [dp, i32, ctypes.POINTER(PlanInfo)]
+    lib.dwconv_plan_candidates.argtypes = [dp, i32, i32, ctypes.POINTER(PlanInfo), ctypes.POINTER(i32)]
+    lib.dwconv_plan_select.argtypes = [dp, i32, i32]
     lib.dwconv_set_variant_override.argtypes = [i32]
     for f in ("dwconv_output_shape", "dwconv_fwd", "dwconv_bwd_data", "dwconv_bwd_filter", "dwconv_bwd",
-              "dwconv_workspace_init", "dwconv_plan", "dwconv_set_variant_override"):
+              "dwconv_workspace_init", "dwconv_plan", "dwconv_plan_candidates", "dwconv_plan_select",
+              "dwconv_set_variant_override"):
         getattr(lib, f).restype = i32
     if lib.dwconv_abi_version() != 1:
         raise RuntimeError("libdwconv ABI version mismatch")

@@ -7,6 +7,7 @@
 #include <climits>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -102,14 +103,30 @@ struct Plan {
 // Choose the kernel family for a pass.  Pure host computation, memoised per
 // (geometry, pass, device, override) because the planner searches many chunkings.
 void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p);
-void make_plan(const Geom& g, int pass, const DevInfo& di, Plan* p) {
-  using Key = std::array<int64_t, 18>;
-  static std::mutex mu;
-  static std::map<Key, Plan> cache;
+
+using PlanKey = std::array<int64_t, 18>;
+PlanKey plan_key(const Geom& g, int pass, const DevInfo& di) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const Key key = {g.N, g.C, g.H, g.W, g.m, g.kh, g.kw, g.sh, g.sw, g.ph, g.pw, g.layout, g.dtype, pass, dev,
-                   g_override.load(), di.sms, 0};
+  return {g.N, g.C, g.H, g.W, g.m, g.kh, g.kw, g.sh, g.sw, g.ph, g.pw, g.layout, g.dtype, pass, dev,
+          g_override.load(), di.sms, 0};
+}
+
+// Plans chosen by measurement (dwconv_plan_select) take precedence over the
+// planner's own pick for the same geometry, pass and device.
+std::mutex g_sel_mu;
+std::map<PlanKey, Plan> g_selected;
+std::map<PlanKey, std::vector<ChunkPlan>> g_candidates;
+
+void make_plan(const Geom& g, int pass, const DevInfo& di, Plan* p) {
+  static std::mutex mu;
+  static std::map<PlanKey, Plan> cache;
+  const PlanKey key = plan_key(g, pass, di);
+  {
+    std::lock_guard<std::mutex> lk(g_sel_mu);
+    auto it = g_selected.find(key);
+    if (it != g_selected.end()) { *p = it->second; return; }
+  }
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
@@ -309,6 +326,78 @@ int dwconv_workspace_init(void* workspace, size_t workspace_bytes, dwconv_stream
   if (workspace_bytes == 0) return DWCONV_OK;
   if (!workspace) return DWCONV_ERR_NULL_POINTER;
   return cuda_status(cudaMemsetAsync(workspace, 0, workspace_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+static void fill_chunk_info(const ChunkPlan& c, dwconv_plan_info* info) {
+  std::memset(info, 0, sizeof(*info));
+  info->variant = DWCONV_VARIANT_NCHW_CHUNK;
+  info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
+  info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
+  info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+}
+
+int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, dwconv_plan_info* infos,
+                           int* count) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if (!count || (max_candidates > 0 && !infos)) return DWCONV_ERR_NULL_POINTER;
+  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD_FILTER || max_candidates < 0) return DWCONV_ERR_BAD_DESCRIPTOR;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  *count = 0;
+  if (g.N == 0 || g.layout != DWCONV_NCHW || g_override.load() == DWCONV_VARIANT_GENERIC) return DWCONV_OK;
+  const PlanKey key = plan_key(g, pass, di);
+  std::vector<ChunkPlan> cands;
+  {
+    std::lock_guard<std::mutex> lk(g_sel_mu);
+    auto it = g_candidates.find(key);
+    if (it != g_candidates.end()) cands = it->second;
+  }
+  if (cands.empty()) {
+    // the planner's own pick (what an unselected call launches) leads the list
+    Plan dp;
+    make_plan_uncached(g, pass, di, &dp);
+    if (dp.variant == DWCONV_VARIANT_NCHW_CHUNK) cands.push_back(dp.chunk);
+    std::vector<ChunkPlan> more;
+    ChunkPlan scratch;
+    if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch, &more, DWCONV_MAX_CANDIDATES) || !more.empty()) {
+      for (const ChunkPlan& c : more) {
+        if ((int)cands.size() >= DWCONV_MAX_CANDIDATES) break;
+        bool dup = false;
+        for (const ChunkPlan& o : cands)
+          dup = dup || (o.P == c.P && o.nbands == c.nbands && o.band_rows == c.band_rows && o.threads == c.threads &&
+                        o.tpg == c.tpg && o.ns == c.ns && o.pair == c.pair && o.direct == c.direct &&
+                        o.nslices == c.nslices && o.grid == c.grid);
+        if (!dup) cands.push_back(c);
+      }
+    }
+    std::lock_guard<std::mutex> lk(g_sel_mu);
+    g_candidates[key] = cands;
+  }
+  const int n = std::min<int>((int)cands.size(), max_candidates);
+  for (int i = 0; i < n; ++i) fill_chunk_info(cands[i], &infos[i]);
+  *count = (max_candidates == 0) ? (int)cands.size() : n;
+  return DWCONV_OK;
+}
+
+int dwconv_plan_select(const dwconv_desc* d, int pass, int index) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD_FILTER) return DWCONV_ERR_BAD_DESCRIPTOR;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  const PlanKey key = plan_key(g, pass, di);
+  std::lock_guard<std::mutex> lk(g_sel_mu);
+  if (index < 0) { g_selected.erase(key); return DWCONV_OK; }
+  auto it = g_candidates.find(key);
+  if (it == g_candidates.end() || index >= (int)it->second.size()) return DWCONV_ERR_BAD_DESCRIPTOR;
+  Plan p;
+  p.variant = DWCONV_VARIANT_NCHW_CHUNK;
+  p.chunk = it->second[(size_t)index];
+  g_selected[key] = p;
+  return DWCONV_OK;
 }
 
 int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {

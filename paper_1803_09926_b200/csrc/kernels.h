@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/dwconv.h"
 
 namespace dwk {
@@ -61,7 +63,10 @@ struct ChunkPlan {
 constexpr int kPassBwdFused = DWCONV_PASS_BWD;  // plan_nchw pass id of the fused backward
 
 // Returns false if the NCHW chunk family cannot handle the geometry.
-bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan);
+// cands: optionally also the distinct candidate plans (default first, then by score),
+// at most max_cands, for measurement-driven selection (dwconv_plan_candidates).
+bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan,
+               std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st);
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,

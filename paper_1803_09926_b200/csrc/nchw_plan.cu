@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "nchw_common.cuh"
 
@@ -147,14 +149,42 @@ double chunk_score(int64_t useful, int64_t slots, int64_t chunk_bytes, int smem,
 
 }  // namespace
 
+// Candidate list for measurement-driven plan selection: the default pick first,
+// then the best-scoring candidate of every distinct chunk shape (planes per
+// chunk, bands, band rows, CTA size / threads per plane, ring depth), in score order.
+template <class Fin>
+static void collect_candidates(std::vector<std::pair<double, ChunkPlan>>& pool, const ChunkPlan* dflt, Fin finalize,
+                               std::vector<ChunkPlan>* out, int max_cands) {
+  std::stable_sort(pool.begin(), pool.end(),
+                   [](const std::pair<double, ChunkPlan>& a, const std::pair<double, ChunkPlan>& b) {
+                     return a.first > b.first;
+                   });
+  auto same = [](const ChunkPlan& a, const ChunkPlan& b) {
+    return a.P == b.P && a.nbands == b.nbands && a.band_rows == b.band_rows && a.threads == b.threads &&
+           a.tpg == b.tpg && a.ns == b.ns && a.pair == b.pair && a.direct == b.direct;
+  };
+  out->clear();
+  if (dflt) out->push_back(*dflt);
+  for (auto& e : pool) {
+    if ((int)out->size() >= max_cands) break;
+    bool dup = false;
+    for (const ChunkPlan& o : *out) dup = dup || same(o, e.second);
+    if (dup) continue;
+    ChunkPlan c = e.second;
+    if (finalize(&c)) out->push_back(c);
+  }
+}
+
 // Register-direct bwd_filter (direct_bwd_filter.cu) for K = 3, pad 1: a row set
 // of L = Wo / V lanes covers an output row, so Wo / V <= 32; rows must be
 // aligned for the vector loads.  Work: P = row sets per warp output channels per
 // CTA (8 row sets each), ~DWCONV_DBF_TASKS tasks (image x strip) per row set.
-static bool plan_direct_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p) {
+static bool plan_direct_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p, int tasks_arg = 0, int max_wo_arg = 0) {
   static const bool on = nchw::env_int("DWCONV_DIRECT_BF", 1, 0, 1) == 1;
-  static const int tasks = nchw::env_int("DWCONV_DBF_TASKS", 4, 1, 64);
-  static const int max_wo = nchw::env_int("DWCONV_DBF_MAXWO", 8, 1, 4096);
+  static const int tasks_env = nchw::env_int("DWCONV_DBF_TASKS", 4, 1, 64);
+  static const int max_wo_env = nchw::env_int("DWCONV_DBF_MAXWO", 8, 1, 4096);
+  const int tasks = tasks_arg > 0 ? tasks_arg : tasks_env;
+  const int max_wo = max_wo_arg > 0 ? max_wo_arg : max_wo_env;
   if (!on || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1 || g.Wo > max_wo) return false;
   const int S = g.sh;
   if (g.sw != S || (S != 1 && S != 2) || g.W != S * g.Wo) return false;
@@ -199,8 +229,14 @@ static bool plan_direct_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p) {
   return p->max_chain <= 160 && groups * nsl < (int64_t)1 << 31;
 }
 
-bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* p) {
+bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* p,
+               std::vector<ChunkPlan>* cands, int max_cands) {
   using namespace nchw;
+  // cands != nullptr: also return up to max_cands distinct chunk shapes, best
+  // score first, for measurement-driven selection (dwconv_plan_candidates);
+  // the search then spans chunk budgets up to 96 KB and both chunk modes.
+  std::vector<std::pair<double, ChunkPlan>> pool;
+  auto keep = [&](double sc, const ChunkPlan& c) { if (cands) pool.emplace_back(sc, c); };
   if (g.layout != DWCONV_NCHW) return false;
   const int K = g.kh;
   if (g.kw != K || (K != 3 && K != 5 && K != 7)) return false;
@@ -214,7 +250,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   if (pass != DWCONV_PASS_BWD_DATA && S * g.Wo > g.W) return false;
   *p = ChunkPlan{};
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
-  const int budget = chunk_budget();
+  const int budget = cands ? 96 * 1024 : chunk_budget();
   const int64_t budget_max = std::max<int64_t>(budget, 48 * 1024);
   const int64_t Q = g.N * g.C;
   const int m = g.m;
@@ -306,6 +342,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       static const double fill_b = 1024.0 * env_int("DWCONV_FILL_KB", 160, 8, 228);
       const double fill_f = std::min(1.0, ctas_eff * c.ns * (double)c.in_bytes / fill_b);
       const double sc = eff * pipe * occ_f * size_f * fill_f;
+      keep(sc, c);
       if (sc > best) { best = sc; bestp = c; }
     };
     if (per <= budget_max) {  // whole-plane chunks
@@ -330,7 +367,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
         }
       }
     }
-    if (best < 0.0 || per > budget) {  // row bands of one plane
+    if (best < 0.0 || per > budget || cands) {  // row bands of one plane
       for (int nsb_b = 1; nsb_b <= nsb_full; ++nsb_b) {
         const int br = nsb_b * R;
         int64_t inb, outb;
@@ -355,22 +392,27 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       }
     }
     if (best < 0.0) return false;
+    auto finalize = [&](ChunkPlan* c) -> bool {
+      c->nchunks = (c->nbands == 1) ? (Q + c->P - 1) / c->P : Q * c->nbands;
+      if (c->nchunks >= ((int64_t)1 << 31)) return false;
+      c->nsb = (c->band_rows + R - 1) / R;
+      KernelFn fn = kernel_for(pass, g.dtype, K, S, c->ri, c->vi, c->padded, c->pair);
+      if (!fn) return false;
+      const int occ = occupancy(fn, c->smem_bytes, c->threads);
+      if (occ < 1) return false;
+      c->grid = (int)std::min<int64_t>(c->nchunks, (int64_t)occ * num_sms);
+      return true;
+    };
     *p = bestp;
-    p->nchunks = (p->nbands == 1) ? (Q + p->P - 1) / p->P : Q * p->nbands;
-    if (p->nchunks >= ((int64_t)1 << 31)) return false;
-    p->nsb = (p->band_rows + R - 1) / R;
-    KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded, p->pair);
-    if (!fn) return false;
-    const int occ = occupancy(fn, p->smem_bytes, p->threads);
-    if (occ < 1) return false;
-    p->grid = (int)std::min<int64_t>(p->nchunks, (int64_t)occ * num_sms);
+    if (!finalize(p)) return false;
+    if (cands) collect_candidates(pool, p, finalize, cands, max_cands);
     return true;
   }
 
   // ---------------- bwd_filter (and the fused backward: + dx from the same staged dy)
   const bool fused = pass == kPassBwdFused;
   if (fused && (g.m != 1 || S != 1 || K != 3)) return false;
-  if (!fused && plan_direct_bwd_filter(g, num_sms, p)) return true;
+  if (!fused && !cands && plan_direct_bwd_filter(g, num_sms, p)) return true;
   const int64_t per = x_plane + y_plane;
   p->ri = (g.Ho % rows_bf(K, 0) == 0) ? 0 : 1;
   p->R = rows_bf(K, p->ri);
@@ -426,6 +468,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     const int64_t groups = (g.C + P - 1) / P;
     const double grp_f = std::min(1.0, (double)groups * std::min<int64_t>(g.N, 32) / (2.0 * num_sms));
     const double sc = chunk_score(useful, slots, xb + dyb, c.smem_bytes, T) * grp_f;
+    keep(sc, c);
     if (sc > best) { best = sc; bestp = c; }
   };
   if (per <= budget_max) {
@@ -436,7 +479,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       for (int tpg = 1; P * m * tpg <= kThreads; ++tpg) consider(P, tpg, 1, (int)g.Ho, P * x_plane, P * y_plane);
     }
   }
-  if (best < 0.0 || per > budget) {
+  if (best < 0.0 || per > budget || cands) {
     for (int nsb_b = 1; nsb_b <= nsb_full; ++nsb_b) {
       const int br = nsb_b * R;
       const int64_t xb = std::min<int64_t>(g.H, (int64_t)(br - 1) * S + K) * g.W * eb;
@@ -448,36 +491,51 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     }
   }
   if (best < 0.0) return false;
+  auto finalize = [&](ChunkPlan* c) -> bool {
+    c->nsb = (c->band_rows + R - 1) / R;
+    c->groups = (int)((g.C + c->P - 1) / c->P);
+    KernelFn fn = kernel_for(pass, g.dtype, K, S, c->ri, c->vi, c->padded);
+    if (!fn) return false;
+    const int occ = occupancy(fn, c->smem_bytes, c->threads);
+    if (occ < 1) return false;
+    const int nb = c->nbands;
+    // batch slices: ~one wave of CTAs, >= 2 chunks per CTA when the batch allows,
+    // <= 32 chunks per CTA (running-sum chain) and <= 128 slices.
+    const int64_t N = std::max<int64_t>(g.N, 1);
+    int64_t nsl = ((int64_t)num_sms * occ + c->groups - 1) / c->groups;  // ~one wave
+    nsl = std::min<int64_t>(nsl, std::max<int64_t>(1, N * nb / 2));
+    nsl = std::max<int64_t>(nsl, (N * nb + 31) / 32);
+    nsl = std::min<int64_t>(nsl, std::min<int64_t>(N, 128));
+    nsl = std::max<int64_t>(nsl, 1);
+    int64_t nps = (N + nsl - 1) / nsl;
+    nsl = (N + nps - 1) / nps;
+    c->nslices = (int)nsl;
+    c->n_per_slice = (int)nps;
+    c->grid = (int)(c->groups * nsl);
+    c->nchunks = (int64_t)c->grid;
+    const bool packed = (S == 1 && c->V % 2 == 0);
+    const int64_t strips_per_thread = ((int64_t)c->nsb * c->ncg + c->tpg - 1) / c->tpg;
+    const int64_t per_chunk = strips_per_thread * R * (packed ? c->V / 2 : c->V) + (packed ? 1 : 0);
+    const int64_t thread_sum = (c->tpg <= 32) ? c->tpg : (c->tpg + 31) / 32 + 5;
+    c->max_chain = (int)(per_chunk + nps * nb + thread_sum + 2 * ilog2_ceil(nsl) + 1);
+    const size_t tick = ((size_t)c->groups * 4 + 15) / 16 * 16;
+    c->ws_bytes = tick + (size_t)nsl * g.C * m * KK * 4;
+    return nsl <= 128 && c->max_chain <= 160;
+  };
   *p = bestp;
-  p->nsb = (p->band_rows + R - 1) / R;
-  p->groups = (int)((g.C + p->P - 1) / p->P);
-  KernelFn fn = kernel_for(pass, g.dtype, K, S, p->ri, p->vi, p->padded);
-  if (!fn) return false;
-  const int occ = occupancy(fn, p->smem_bytes, p->threads);
-  if (occ < 1) return false;
-  const int nb = p->nbands;
-  // batch slices: ~one wave of CTAs, >= 2 chunks per CTA when the batch allows,
-  // <= 32 chunks per CTA (running-sum chain) and <= 128 slices.
-  const int64_t N = std::max<int64_t>(g.N, 1);
-  int64_t nsl = ((int64_t)num_sms * occ + p->groups - 1) / p->groups;  // ~one wave
-  nsl = std::min<int64_t>(nsl, std::max<int64_t>(1, N * nb / 2));
-  nsl = std::max<int64_t>(nsl, (N * nb + 31) / 32);
-  nsl = std::min<int64_t>(nsl, std::min<int64_t>(N, 128));
-  nsl = std::max<int64_t>(nsl, 1);
-  int64_t nps = (N + nsl - 1) / nsl;
-  nsl = (N + nps - 1) / nps;
-  p->nslices = (int)nsl;
-  p->n_per_slice = (int)nps;
-  p->grid = (int)(p->groups * nsl);
-  p->nchunks = (int64_t)p->grid;
-  const bool packed = (S == 1 && p->V % 2 == 0);
-  const int64_t strips_per_thread = ((int64_t)p->nsb * p->ncg + p->tpg - 1) / p->tpg;
-  const int64_t per_chunk = strips_per_thread * R * (packed ? p->V / 2 : p->V) + (packed ? 1 : 0);
-  const int64_t thread_sum = (p->tpg <= 32) ? p->tpg : (p->tpg + 31) / 32 + 5;
-  p->max_chain = (int)(per_chunk + nps * nb + thread_sum + 2 * ilog2_ceil(nsl) + 1);
-  const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
-  p->ws_bytes = tick + (size_t)nsl * g.C * m * KK * 4;
-  return nsl <= 128;
+  const bool ok = finalize(p);
+  if (cands) {
+    collect_candidates(pool, ok ? p : nullptr, finalize, cands, max_cands);
+    if (!fused) {  // register-direct variants (no smem staging) compete too
+      for (int tasks : {2, 4}) {
+        ChunkPlan d;
+        if (plan_direct_bwd_filter(g, num_sms, &d, tasks, 4096)) cands->push_back(d);
+      }
+      ChunkPlan d0;  // the default planner's pick leads the list
+      if (plan_direct_bwd_filter(g, num_sms, &d0)) cands->insert(cands->begin(), d0);
+    }
+  }
+  return ok;
 }
 
 // Launch with programmatic dependent launch allowed (the kernels call

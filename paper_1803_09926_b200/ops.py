@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
-from typing import Dict, Optional, Sequence, Tuple, Union
+from typing import Dict, List, Optional, Sequence, Tuple, Union
 
 import torch
 
@@ -136,6 +136,25 @@ def dwconv_plan(d: Desc, pass_: int) -> Dict[str, int]:
     out = {f: getattr(info, f) for f, _ in PlanInfo._fields_}
     out["variant_name"] = _lib.VARIANTS.get(info.variant, "?")
     return out
+
+
+def dwconv_plan_candidates(d: Desc, pass_: int, max_candidates: int = _lib.MAX_CANDIDATES) -> List[Dict[str, int]]:
+    """Distinct NCHW launch shapes for (d, pass_), the planner's default first (include/dwconv.h)."""
+    infos = (PlanInfo * max(1, max_candidates))()
+    count = ctypes.c_int32(0)
+    _lib.check(_lib.load().dwconv_plan_candidates(ctypes.byref(d), pass_, max_candidates, infos,
+                                                  ctypes.byref(count)), "dwconv_plan_candidates")
+    out = []
+    for i in range(count.value):
+        e = {f: getattr(infos[i], f) for f, _ in PlanInfo._fields_}
+        e["variant_name"] = _lib.VARIANTS.get(infos[i].variant, "?")
+        out.append(e)
+    return out
+
+
+def dwconv_plan_select(d: Desc, pass_: int, index: int) -> None:
+    """Install candidate `index` of dwconv_plan_candidates for (d, pass_); -1 restores the default."""
+    _lib.check(_lib.load().dwconv_plan_select(ctypes.byref(d), pass_, index), "dwconv_plan_select")
 
 
 def dwconv_set_variant_override(v: int) -> None:

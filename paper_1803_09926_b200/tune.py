@@ -1,0 +1,99 @@
+"""Measurement-driven plan selection for the NCHW chunk kernels (a "find" step).
+
+The planner in ``csrc/nchw_plan.cu`` scores chunk shapes with a cost model;
+on B200 the best launch shape of a memory-bound stencil also depends on DRAM
+page locality, L2 behaviour and ramp/tail effects the model does not see (a
+sweep of dw2 bwd_filter spans 42-120 us over shapes the model ranks close).
+``tune_layer`` times every candidate the library offers
+(``dwconv_plan_candidates``) on the caller's tensors and installs the fastest
+(``dwconv_plan_select``).  Host-side orchestration only: every launch it times
+is the library's own kernel; nothing here computes a result.
+
+Timing follows bench.py: back-to-back launches from a CUDA graph, cycling over
+copies of the pass's tensors whose footprint is >= 2x L2, CUDA events on the
+launching stream.  A candidate replaces the planner's default only if it is
+faster by more than ``min_gain``.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional
+
+import torch
+
+from . import ops
+from ._lib import NCHW, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_FWD
+
+PASSES = {"fwd": PASS_FWD, "bwd_data": PASS_BWD_DATA, "bwd_filter": PASS_BWD_FILTER}
+
+
+def _graph_us(calls, reps: int, stream: torch.cuda.Stream) -> float:
+    with torch.cuda.stream(stream):
+        for c in calls:
+            c()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for c in calls:
+                c()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    del g
+    return e0.elapsed_time(e1) * 1e3 / (reps * len(calls))
+
+
+def tune_layer(d, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, passes=("fwd", "bwd_data", "bwd_filter"),
+               reps: int = 3, min_gain: float = 0.02, stream: Optional[torch.cuda.Stream] = None) -> Dict[str, dict]:
+    """Select the fastest candidate plan of each pass for descriptor ``d`` (NCHW only).
+
+    x, dy, w: the layer's tensors (their values are not modified).  Returns, per
+    pass, the chosen index, its time and the default's time (microseconds).
+    """
+    out: Dict[str, dict] = {}
+    if d.layout != NCHW or d.n == 0:
+        return out
+    dev = x.device
+    stream = stream or torch.cuda.Stream(device=dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    set_bytes = sum(t.numel() * t.element_size() for t in (x, dy)) * 2
+    nsets = int(max(2, min(8, -(-2 * l2 // set_bytes))))
+    sets = [dict(x=x, dy=dy)] + [dict(x=x.clone(), dy=dy.clone()) for _ in range(nsets - 1)]
+    for s in sets:
+        s["y"] = torch.empty_like(dy)
+        s["dx"] = torch.empty_like(x)
+    dw = torch.empty(w.shape, dtype=torch.float32, device=dev)
+    for name in passes:
+        p = PASSES[name]
+        cands: List[dict] = ops.dwconv_plan_candidates(d, p)
+        if len(cands) <= 1:
+            continue
+        ws = None
+        if p == PASS_BWD_FILTER:
+            ws = torch.zeros(max(16, max(c["workspace_bytes"] for c in cands)), dtype=torch.uint8, device=dev)
+
+        def mk(s):
+            if p == PASS_FWD:
+                return lambda: ops.dwconv_fwd(d, s["x"], w, s["y"])
+            if p == PASS_BWD_DATA:
+                return lambda: ops.dwconv_bwd_data(d, s["dy"], w, s["dx"])
+            return lambda: ops.dwconv_bwd_filter(d, s["x"], s["dy"], dw, ws)
+
+        times = []
+        for i in range(len(cands)):
+            ops.dwconv_plan_select(d, p, i)
+            times.append(_graph_us([mk(s) for s in sets * 2], reps, stream))
+        best = min(range(len(times)), key=lambda i: times[i])
+        if times[best] > times[0] * (1.0 - min_gain):
+            best = 0
+        ops.dwconv_plan_select(d, p, best)
+        out[name] = {"index": best, "us": times[best], "default_us": times[0], "candidates": len(cands),
+                     "grid": cands[best]["grid"], "block": cands[best]["block"],
+                     "planes_per_chunk": cands[best]["planes_per_chunk"],
+                     "rows_per_band": cands[best]["rows_per_band"]}
+        del ws
+    return out
