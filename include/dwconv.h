@@ -155,7 +155,8 @@ typedef enum {
   DWCONV_VARIANT_NONE = 0,        /* empty batch: nothing to launch (bwd_filter: a memset)  */
   DWCONV_VARIANT_GENERIC = 1,     /* any shape: one thread per output element, global loads */
   DWCONV_VARIANT_NCHW_CHUNK = 2,  /* NCHW: whole planes / row bands staged by bulk TMA      */
-  DWCONV_VARIANT_NHWC_TILE = 3    /* NHWC: spatial x channel tiles staged by TMA            */
+  DWCONV_VARIANT_NHWC_TILE = 3,   /* NHWC: spatial x channel-vector register tiles, L1 loads */
+  DWCONV_VARIANT_NHWC_TMA = 4     /* NHWC: 4-D tensor-map TMA boxes with zero-filled halos  */
 } dwconv_variant;
 typedef struct {
   int32_t variant;            /* dwconv_variant */

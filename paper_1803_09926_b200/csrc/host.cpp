@@ -98,6 +98,7 @@ struct Plan {
   int variant = DWCONV_VARIANT_NONE;
   ChunkPlan chunk{};
   NhwcPlan nhwc{};
+  dwk::NhwcTmaPlan tma{};
 };
 
 // Choose the kernel family for a pass.  Pure host computation, memoised per
@@ -150,12 +151,22 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
     if (p->variant != DWCONV_VARIANT_NCHW_CHUNK || g.dtype != DWCONV_F32) p->variant = DWCONV_VARIANT_NONE;
     return;
   }
+  if (g.layout == DWCONV_NHWC && dwk::plan_nhwc_tma(g, pass, di.sms, di.smem_optin, &p->tma)) {
+    p->variant = DWCONV_VARIANT_NHWC_TMA;
+    dwk::plan_nhwc(g, pass, di.sms, &p->nhwc);  // for unaligned pointers
+    return;
+  }
   if (g.layout == DWCONV_NHWC && dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->variant = DWCONV_VARIANT_NHWC_TILE;
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? DWCONV_OK : DWCONV_ERR_CUDA; }
 
 // the NHWC kernels move 4-channel vectors: 16-B (fp32) / 8-B (bf16) aligned activations
+// tensor-map base and 16-B vector stores (fp32) / 8-B (bf16)
+bool tma_aligned(const void* in, const void* out) {
+  return ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16) == 0;
+}
+
 bool nhwc_aligned(const Geom& g, const void* a, const void* b) {
   const uintptr_t al = (g.dtype == DWCONV_F32) ? 16 : 8;
   return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % al) == 0;
@@ -214,7 +225,10 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
   // the NCHW kernels store y with V-wide vector stores straight from registers
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(y) % 16) == 0)
     return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
-  if (p.variant == DWCONV_VARIANT_NHWC_TILE && nhwc_aligned(g, x, y))
+  if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(x, y))
+    return cuda_status(dwk::launch_nhwc_tma(g, p.tma, x, w, y, st));
+  if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
+      nhwc_aligned(g, x, y))
     return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_FWD, x, w, y, st));
   return cuda_status(dwk::launch_generic_fwd(g, x, w, y, st));
 }
@@ -236,7 +250,10 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
   // the NCHW kernels store dx with vector stores straight from registers
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0)
     return cuda_status(dwk::launch_nchw_bwd_data(g, p.chunk, dy, w, dx, st));
-  if (p.variant == DWCONV_VARIANT_NHWC_TILE && nhwc_aligned(g, dy, dx))
+  if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(dy, dx))
+    return cuda_status(dwk::launch_nhwc_tma(g, p.tma, dy, w, dx, st));
+  if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
+      nhwc_aligned(g, dy, dx))
     return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_BWD_DATA, dy, w, dx, st));
   return cuda_status(dwk::launch_generic_bwd_data(g, dy, w, dx, st));
 }
@@ -422,6 +439,10 @@ int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
     info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
     info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+  } else if (p.variant == DWCONV_VARIANT_NHWC_TMA) {
+    const dwk::NhwcTmaPlan& c = p.tma;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
+    info->work_units = c.ntiles; info->rows_per_band = c.TH; info->planes_per_chunk = c.TW;
   } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
     const NhwcPlan& c = p.nhwc;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;

@@ -93,4 +93,17 @@ cudaError_t launch_nhwc_fd(const Geom& g, const NhwcPlan& p, int pass, const voi
 cudaError_t launch_nhwc_bwd_filter(const Geom& g, const NhwcPlan& p, const void* x, const void* dy, float* dw,
                                    void* ws, cudaStream_t st);
 
+// ---- NHWC fwd / bwd_data from tensor-map TMA tiles (m = 1, 3x3, pad 1, S in {1,2}): nhwc_tma.cu
+struct NhwcTmaPlan {
+  int mode;               // 0 fwd s1, 1 fwd s2, 2 bwd_data s1, 3 bwd_data s2
+  int threads, grid, smem, ns;
+  int TH, TW, CB, NCV, BW, BH, cons;
+  int tiles_h, tiles_w, ncb;
+  int64_t ntiles;
+  uint32_t box_bytes, stage_bytes;
+};
+bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* plan);
+cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in, const void* w, void* out,
+                            cudaStream_t st);
+
 }  // namespace dwk

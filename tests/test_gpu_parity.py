@@ -232,6 +232,9 @@ NHWC_FAST = [
     (2, 24, 15, 9, 1, 3, 2, 1),     # CV = 6, stride 2, odd sizes
     (1, 1028, 7, 7, 1, 3, 1, 1),    # CV = 257 > 256: two channel groups in bwd_filter
     (2, 64, 28, 28, 1, 3, 2, 1),
+    (2, 96, 30, 30, 1, 3, 1, 1),    # TMA tiles: ragged 16-wide columns, 7/8-row tiles
+    (2, 96, 30, 34, 1, 3, 2, 1),    # TMA stride 2: odd output widths, ragged tiles
+    (1, 256, 9, 21, 1, 3, 2, 1),    # TMA bwd_data polyphase: odd H, W (dx rows/columns past the last dy)
 ]
 
 
@@ -241,8 +244,9 @@ def test_nhwc_fast_path(shape, dtype, _lib):
     import paper_1803_09926_b200.ops as ops
     n, c, h, w, m, k, s, p = shape
     d = ops.make_desc(n, c, h, w, m, k, s, p, NHWC, 0 if dtype == "f32" else 1)
-    for pas in (0, 1, 2):
-        assert ops.dwconv_plan(d, pas)["variant_name"] == "nhwc_tile", (shape, pas)
+    for pas in (0, 1):
+        assert ops.dwconv_plan(d, pas)["variant_name"] in ("nhwc_tile", "nhwc_tma"), (shape, pas)
+    assert ops.dwconv_plan(d, 2)["variant_name"] == "nhwc_tile", shape
     check_all(*shape, layout=NHWC, dtype=dtype, kind="unif")
     check_all(*shape, layout=NHWC, dtype=dtype, kind="int", amax=2 if dtype == "bf16" else 3)
 
