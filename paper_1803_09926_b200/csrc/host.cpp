@@ -151,9 +151,15 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
     if (p->variant != DWCONV_VARIANT_NCHW_CHUNK || g.dtype != DWCONV_F32) p->variant = DWCONV_VARIANT_NONE;
     return;
   }
+  if (g.layout == DWCONV_NHWC && pass == DWCONV_PASS_BWD_FILTER &&
+      dwk::plan_nhwc_tma_bf(g, di.sms, di.smem_optin, &p->tma)) {
+    p->variant = DWCONV_VARIANT_NHWC_TMA;
+    if (!dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->nhwc = NhwcPlan{};  // for unaligned pointers
+    return;
+  }
   if (g.layout == DWCONV_NHWC && dwk::plan_nhwc_tma(g, pass, di.sms, di.smem_optin, &p->tma)) {
     p->variant = DWCONV_VARIANT_NHWC_TMA;
-    dwk::plan_nhwc(g, pass, di.sms, &p->nhwc);  // for unaligned pointers
+    if (!dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->nhwc = NhwcPlan{};  // for unaligned pointers
     return;
   }
   if (g.layout == DWCONV_NHWC && dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->variant = DWCONV_VARIANT_NHWC_TILE;
@@ -266,6 +272,8 @@ size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
   Plan p;
   make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
   if (p.variant == DWCONV_VARIANT_NHWC_TILE) return p.nhwc.ws_bytes;
+  if (p.variant == DWCONV_VARIANT_NHWC_TMA)  // either NHWC kernel may run (pointer alignment)
+    return std::max(p.tma.ws_bytes, p.nhwc.grid > 0 ? p.nhwc.ws_bytes : (size_t)0);
   return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? p.chunk.ws_bytes : 0;
 }
 
@@ -293,7 +301,14 @@ int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float
     if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
     return cuda_status(dwk::launch_nchw_bwd_filter(g, p.chunk, x, dy, dw, workspace, st));
   }
-  if (p.variant == DWCONV_VARIANT_NHWC_TILE && nhwc_aligned(g, x, dy)) {
+  if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(x, dy)) {
+    if (workspace_bytes < p.tma.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
+    if (!workspace) return DWCONV_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
+    return cuda_status(dwk::launch_nhwc_tma_bf(g, p.tma, x, dy, dw, workspace, st));
+  }
+  if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
+      nhwc_aligned(g, x, dy)) {
     if (workspace_bytes < p.nhwc.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
     if (!workspace) return DWCONV_ERR_NULL_POINTER;
     if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
@@ -443,6 +458,10 @@ int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
     const dwk::NhwcTmaPlan& c = p.tma;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
     info->work_units = c.ntiles; info->rows_per_band = c.TH; info->planes_per_chunk = c.TW;
+    if (pass == DWCONV_PASS_BWD_FILTER) {
+      info->work_units = (int64_t)c.ncb * c.tiles_per_cb;
+      info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+    }
   } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
     const NhwcPlan& c = p.nhwc;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;

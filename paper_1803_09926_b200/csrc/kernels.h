@@ -101,9 +101,16 @@ struct NhwcTmaPlan {
   int tiles_h, tiles_w, ncb;
   int64_t ntiles;
   uint32_t box_bytes, stage_bytes;
+  // bwd_filter (mode 5 / 6 = stride 1 / 2)
+  uint32_t dy_bytes, dy_off;
+  int tiles_per_cb, nslices, tps, max_chain;
+  size_t ws_bytes;
 };
 bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* plan);
 cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in, const void* w, void* out,
                             cudaStream_t st);
+bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* plan);
+cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* x, const void* dy, float* dw,
+                               void* ws, cudaStream_t st);
 
 }  // namespace dwk

@@ -27,6 +27,9 @@
 //     dy 2x2 neighbourhood (a..a+1, b..b+1); the dy box starts at (oh0/2, ow0/2).
 #include <cuda.h>
 
+#include <mutex>
+#include <vector>
+
 #include "kernels.h"
 #include "nchw_common.cuh"
 
@@ -255,6 +258,218 @@ __global__ void __launch_bounds__(kMaxConsumers + 32) nhwc_tma_kernel(const __gr
   if (!a.early_pdl) griddep_launch_dependents();
 }
 
+// ---------------------------------------------------------------- bwd_filter
+// dw[c, i, j] = sum_{n, oh, ow} x[n, oh*S-1+i, ow*S-1+j, c] * dy[n, oh, ow, c]
+// (the block diagonal Eq. 4 keeps, summed over the batch:
+// reading R5).  A stage holds the tile's x box (zero-filled halo) and its dy box
+// (zero-filled past the edges, so ragged tiles add exact zeros).  CTA = (channel
+// block, slice of the block's tiles); consumer thread = (channel vector, tile
+// column), walking the TH rows with the forward's sliding x window.
+// Deterministic reduction, fixed order everywhere:
+//   per tile (TH terms, FFMA2) -> running sum over the CTA's tiles (<= 64)
+//   -> tile columns pairwise -> per-slice partial in the workspace; the last CTA
+//   of the channel block (integer ticket) sums the slices pairwise in slice
+//   order and re-zeroes the workspace.  No float atomics.
+struct BArgs {
+  float* dw;
+  float* ws_part;
+  unsigned* ws_ticket;
+  int N, C, CB, NCV, TW;
+  int tiles_h, tiles_w, ncb, nslices, tps;
+  int tiles_per_cb;
+  int BW, DBW;  // x box width, dy box width (pixels)
+  uint32_t x_bytes, dy_bytes, dy_off, stage_bytes;
+  int ns, cons;
+  int early_pdl;
+};
+
+template <class T, int S, int TH>
+__global__ void __launch_bounds__(kMaxConsumers + 32) nhwc_tma_bf_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                                          const __grid_constant__ CUtensorMap tmd,
+                                                                          const BArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 64);
+  const int nwarps_c = (a.cons + 31) >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], nwarps_c);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_wait();
+  const int g = blockIdx.x % a.ncb;
+  const int sl = blockIdx.x / a.ncb;
+  const int t0 = sl * a.tps;
+  const int t1 = min(a.tiles_per_cb, t0 + a.tps);
+  auto sx = [&](int s) { return reinterpret_cast<T*>(smem + 128 + (size_t)s * a.stage_bytes); };
+  auto sd = [&](int s) { return reinterpret_cast<T*>(smem + 128 + (size_t)s * a.stage_bytes + a.dy_off); };
+  auto dec = [&](int t, int* n, int* oh0, int* ow0) {
+    const int q1 = t / a.tiles_w;
+    *ow0 = (t - q1 * a.tiles_w) * a.TW;
+    const int q2 = q1 / a.tiles_h;
+    *oh0 = (q1 - q2 * a.tiles_h) * TH;
+    *n = q2;
+  };
+  const int ctid = (int)threadIdx.x - 32;
+  const int cv = ctid % a.NCV;
+  const int col = ctid / a.NCV;
+  const bool live = ctid >= 0 && ctid < a.cons && col < a.TW;
+  float2 run[9][2];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) run[q][0] = run[q][1] = make_float2(0.f, 0.f);
+
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {  // producer
+      int s = 0, it = 0;
+      uint32_t ph = 0;
+      for (int t = t0; t < t1; ++t, ++it) {
+        if (it >= a.ns) mbar_wait(&empty[s], ph ^ 1);
+        int n, oh0, ow0;
+        dec(t, &n, &oh0, &ow0);
+        mbar_arrive_expect_tx(&full[s], a.x_bytes + a.dy_bytes);
+        tma_load_4d(sx(s), &tmx, g * a.CB, ow0 * S - 1, oh0 * S - 1, n, &full[s]);
+        tma_load_4d(sd(s), &tmd, g * a.CB, ow0, oh0, n, &full[s]);
+        if (++s == a.ns) { s = 0; ph ^= 1; }
+      }
+      if (a.early_pdl) griddep_launch_dependents();
+    }
+  } else {
+    int s = 0;
+    uint32_t ph = 0;
+    const int rowS = a.BW * a.CB, drowS = a.DBW * a.CB, CB = a.CB;
+    for (int t = t0; t < t1; ++t) {
+      mbar_wait(&full[s], ph);
+      if (live) {
+        const T* pr = sx(s) + cv * VC + col * S * CB;
+        const T* pd = sd(s) + cv * VC + col * CB;
+        float2 xw[3][3][2];
+#pragma unroll
+        for (int r = 0; r < 3 - S; ++r) {
+#pragma unroll
+          for (int j = 0; j < 3; ++j) ld4<T>(pr + j * CB, xw[r][j][0], xw[r][j][1]);
+          pr += rowS;
+        }
+        float2 loc[9][2];
+#pragma unroll
+        for (int r = 0; r < TH; ++r) {
+#pragma unroll
+          for (int rr = 3 - S; rr < 3; ++rr) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) ld4<T>(pr + j * CB, xw[rr][j][0], xw[rr][j][1]);
+            pr += rowS;
+          }
+          float2 dv[2];
+          ld4<T>(pd, dv[0], dv[1]);
+          pd += drowS;
+#pragma unroll
+          for (int q = 0; q < 9; ++q)
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              loc[q][v] = (r == 0) ? __fmul2_rn(xw[q / 3][q % 3][v], dv[v])
+                                   : __ffma2_rn(xw[q / 3][q % 3][v], dv[v], loc[q][v]);
+#pragma unroll
+          for (int rr = 0; rr < 3 - S; ++rr)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) xw[rr][j][v] = xw[rr + S][j][v];
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) run[q][v] = __fadd2_rn(run[q][v], loc[q][v]);
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+      if (++s == a.ns) { s = 0; ph ^= 1; }
+    }
+  }
+  if (!a.early_pdl) griddep_launch_dependents();
+  // ---- every stage has been consumed (no TMA write is pending): reuse the ring
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem + 128);  // [col][cv][q*4 + ch]
+  if (live) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      float* d = red + ((int64_t)col * a.NCV + cv) * 36 + q * 4;
+      d[0] = run[q][0].x; d[1] = run[q][0].y; d[2] = run[q][1].x; d[3] = run[q][1].y;
+    }
+  }
+  __syncthreads();
+  const int C = a.C;
+  float* part = a.ws_part + (int64_t)sl * C * 9;
+  for (int e = threadIdx.x; e < a.NCV * 36; e += blockDim.x) {
+    const int cvv = e / 36, rem = e - cvv * 36;
+    const int q = rem >> 2, ch = rem & 3;
+    float stk[8];
+    int top = 0;
+    for (int c2 = 0; c2 < a.TW; ++c2) {  // tile columns pairwise (binary counter)
+      float cur = red[((int64_t)c2 * a.NCV + cvv) * 36 + rem];
+      int bits = c2;
+      while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+      stk[top++] = cur;
+    }
+    float tot = stk[--top];
+    while (top > 0) tot = stk[--top] + tot;
+    part[(int64_t)(g * a.CB + cvv * VC + ch) * 9 + q] = tot;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
+    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int64_t e0 = (int64_t)g * a.CB * 9;
+    const int nvals = a.CB * 9;
+    const int64_t sstride = (int64_t)C * 9;
+    for (int idx = threadIdx.x; idx < nvals; idx += blockDim.x) {
+      float stk[16];
+      int top = 0;
+      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
+        float vals[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int s2 = s0 + u;
+          if (s2 < a.nslices) {
+            float cur = vals[u];
+            int bits = s2;
+            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+            stk[top++] = cur;
+          }
+        }
+      }
+      float tot = stk[--top];
+      while (top > 0) tot = stk[--top] + tot;
+      a.dw[e0 + idx] = tot;
+    }
+    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  }
+}
+
+using BKernelFn = void (*)(const CUtensorMap, const CUtensorMap, const BArgs);
+BKernelFn bf_kernel_for(int dtype, int S, int TH) {
+  if (dtype == DWCONV_F32) {
+    if (S == 1) return TH == 7 ? nhwc_tma_bf_kernel<float, 1, 7> : nhwc_tma_bf_kernel<float, 1, 8>;
+    return TH == 7 ? nhwc_tma_bf_kernel<float, 2, 7> : nhwc_tma_bf_kernel<float, 2, 8>;
+  }
+  using B = __nv_bfloat16;
+  if (S == 1) return TH == 7 ? nhwc_tma_bf_kernel<B, 1, 7> : nhwc_tma_bf_kernel<B, 1, 8>;
+  return TH == 7 ? nhwc_tma_bf_kernel<B, 2, 7> : nhwc_tma_bf_kernel<B, 2, 8>;
+}
+
 using TKernelFn = void (*)(const CUtensorMap, const TArgs);
 
 template <class T, int MODE>
@@ -293,6 +508,24 @@ EncodeFn encode_fn() {
     return reinterpret_cast<EncodeFn>(p);
   }();
   return fn;
+}
+
+// Opt a kernel in to the largest dynamic shared memory it can use (the opt-in
+// limit minus its static shared memory), once: the attribute is per function, so
+// every plan of that kernel must fit under the same setting.
+bool allow_max_smem(const void* fn, int smem_optin) {
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const void* f : done)
+    if (f == fn) return true;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - (int)fa.sharedSizeBytes) !=
+      cudaSuccess)
+    return false;
+  done.push_back(fn);
+  return true;
 }
 
 int env_int(const char* name, int dflt, int lo, int hi) {
@@ -366,11 +599,11 @@ bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTma
   p->ns = ns_want;
   while (p->ns > 2 && 128 + (int64_t)p->ns * p->stage_bytes > smem_optin) --p->ns;
   p->smem = (int)(128 + p->ns * p->stage_bytes);
-  if (p->smem > smem_optin) return false;
+  if (p->smem > smem_optin - 1024) return false;
   TKernelFn fn = kernel_for(g.dtype, p->mode, TH);
   if (!fn) return false;
   p->threads = 32 + ((p->cons + 31) / 32) * 32;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  if (!allow_max_smem(reinterpret_cast<const void*>(fn), smem_optin)) return false;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p->threads, p->smem) != cudaSuccess || occ < 1)
     return false;
@@ -421,6 +654,148 @@ cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in,
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, fn, tm, a);
+}
+
+bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p) {
+  using namespace nhwct;
+  static const int on = env_int("DWCONV_NHWC_TMA", 1, 0, 1);
+  if (!on || g.layout != DWCONV_NHWC || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
+  const int S = g.sh;
+  if (g.sw != S || (S != 1 && S != 2)) return false;
+  if (!encode_fn()) return false;
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  if ((g.C * eb) % 16 != 0 || g.C % VC != 0) return false;
+  if (g.N > INT32_MAX || g.H > 65535 || g.W > 65535) return false;
+  *p = NhwcTmaPlan{};
+  p->mode = 4 + S;  // bwd_filter
+  int64_t CB = std::min<int64_t>(g.C, 128 / eb);
+  while (CB > VC && (g.C % CB != 0 || CB % VC != 0)) CB -= VC;
+  if (g.C % CB != 0 || (CB * eb) % 16 != 0) return false;
+  const int NCV = (int)(CB / VC);
+  const int TH = (g.Ho % 7 == 0) ? 7 : 8;
+  static const int tw_env = env_int("DWCONV_NHWC_TW", 16, 1, 64);
+  const int tw_cap = std::max(1, std::min(tw_env, kMaxConsumers / NCV));
+  int TW = 0;
+  for (int t = (int)std::min<int64_t>(g.Wo, tw_cap); t >= 1; --t)
+    if (g.Wo % t == 0) { TW = t; break; }
+  if (TW < tw_cap / 2 && g.Wo > tw_cap) TW = tw_cap;
+  static const int ns_want = env_int("DWCONV_NHWC_STAGES", 4, 2, 8);
+  auto sizes = [&](int tw, int* bw, int* bh, uint32_t* xb, uint32_t* db) {
+    *bw = (tw - 1) * S + 3; *bh = (TH - 1) * S + 3;
+    *xb = (uint32_t)(CB * *bw * *bh * eb);
+    *db = (uint32_t)(CB * tw * TH * eb);
+  };
+  int BW, BH;
+  uint32_t xb, db;
+  sizes(TW, &BW, &BH, &xb, &db);
+  // a shallower ring before narrower tiles (consumer threads = NCV x TW): keep
+  // the CTA's ring <= ~100 KB so two CTAs share an SM
+  int ns_fit = ns_want;
+  while (ns_fit > 2 && (int64_t)ns_fit * (xb + db) > 100 * 1024) --ns_fit;
+  while ((int64_t)ns_fit * (xb + db) > 100 * 1024 && TW > 4) {
+    int t = TW - 1;
+    while (t > 4 && g.Wo % t != 0) --t;
+    TW = t;
+    sizes(TW, &BW, &BH, &xb, &db);
+  }
+  if (BW > 256 || BH > 256 || TW > 256) return false;
+  p->TH = TH; p->TW = TW; p->CB = (int)CB; p->NCV = NCV; p->BW = BW; p->BH = BH;
+  p->cons = NCV * TW;
+  p->box_bytes = xb;
+  p->dy_bytes = db;
+  p->dy_off = (xb + 127u) & ~127u;
+  p->stage_bytes = (p->dy_off + db + 127u) & ~127u;
+  p->tiles_h = (int)((g.Ho + TH - 1) / TH);
+  p->tiles_w = (int)((g.Wo + TW - 1) / TW);
+  p->ncb = (int)(g.C / CB);
+  const int64_t tpc = g.N * p->tiles_h * p->tiles_w;
+  if (tpc >= ((int64_t)1 << 31) || tpc < 1) return false;
+  p->tiles_per_cb = (int)tpc;
+  p->ns = ns_fit;
+  const uint32_t red_bytes = (uint32_t)(TW * NCV * 36 * 4);
+  while (p->ns > 2 && 128 + (int64_t)p->ns * p->stage_bytes > smem_optin) --p->ns;
+  p->smem = (int)(128 + std::max<uint32_t>(p->ns * p->stage_bytes, red_bytes));
+  if (p->smem > smem_optin - 1024) return false;
+  BKernelFn fn = bf_kernel_for(g.dtype, S, TH);
+  p->threads = 32 + ((p->cons + 31) / 32) * 32;
+  if (!allow_max_smem(reinterpret_cast<const void*>(fn), smem_optin)) return false;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p->threads, p->smem) != cudaSuccess || occ < 1)
+    return false;
+  // slices: one full wave of CTAs, <= 64 tiles per CTA (running-sum chain), <= 1024 slices
+  int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->ncb);
+  nsl = std::max<int64_t>(nsl, (tpc + 63) / 64);
+  nsl = std::min<int64_t>(nsl, std::min<int64_t>(tpc, 1024));
+  int64_t tps = (tpc + nsl - 1) / nsl;
+  nsl = (tpc + tps - 1) / tps;
+  if (tps > 64) return false;
+  p->nslices = (int)nsl;
+  p->tps = (int)tps;
+  p->grid = (int)(p->ncb * nsl);
+  int lt = 0;
+  while ((1 << lt) < TW) ++lt;
+  int ls = 0;
+  while ((1ll << ls) < nsl) ++ls;
+  p->max_chain = TH + (int)tps + lt + 2 * ls + 1;
+  const size_t tick = ((size_t)p->ncb * 4 + 15) / 16 * 16;
+  p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
+  return p->max_chain <= 160;
+}
+
+cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* x, const void* dy, float* dw,
+                               void* ws, cudaStream_t st) {
+  using namespace nhwct;
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  EncodeFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const CUtensorMapDataType dt = g.dtype == DWCONV_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUtensorMap tmx, tmd;
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    const cuuint64_t str[3] = {(cuuint64_t)(g.C * eb), (cuuint64_t)(g.C * g.W * eb), (cuuint64_t)(g.C * g.W * g.H * eb)};
+    const cuuint32_t box[4] = {(cuuint32_t)p.CB, (cuuint32_t)p.BW, (cuuint32_t)p.BH, 1};
+    if (enc(&tmx, dt, 4, const_cast<void*>(x), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.Wo, (cuuint64_t)g.Ho, (cuuint64_t)g.N};
+    const cuuint64_t str[3] = {(cuuint64_t)(g.C * eb), (cuuint64_t)(g.C * g.Wo * eb),
+                               (cuuint64_t)(g.C * g.Wo * g.Ho * eb)};
+    const cuuint32_t box[4] = {(cuuint32_t)p.CB, (cuuint32_t)p.TW, (cuuint32_t)p.TH, 1};
+    if (enc(&tmd, dt, 4, const_cast<void*>(dy), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  BArgs a{};
+  a.dw = dw;
+  const size_t tick = ((size_t)p.ncb * 4 + 15) / 16 * 16;
+  a.ws_ticket = static_cast<unsigned*>(ws);
+  a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
+  a.N = (int)g.N; a.C = (int)g.C; a.CB = p.CB; a.NCV = p.NCV; a.TW = p.TW;
+  a.tiles_h = p.tiles_h; a.tiles_w = p.tiles_w; a.ncb = p.ncb; a.nslices = p.nslices; a.tps = p.tps;
+  a.tiles_per_cb = p.tiles_per_cb;
+  a.BW = p.BW; a.DBW = p.TW;
+  a.x_bytes = p.box_bytes; a.dy_bytes = p.dy_bytes; a.dy_off = p.dy_off; a.stage_bytes = p.stage_bytes;
+  a.ns = p.ns; a.cons = p.cons;
+  static const int early = env_int("DWCONV_EARLY_PDL", 1, 0, 1);
+  a.early_pdl = early;
+  BKernelFn fn = bf_kernel_for(g.dtype, (int)g.sh, p.TH);
+  static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.grid);
+  cfg.blockDim = dim3((unsigned)p.threads);
+  cfg.dynamicSmemBytes = (size_t)p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, tmx, tmd, a);
 }
 
 }  // namespace dwk
