@@ -97,3 +97,17 @@ def tune_layer(d, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, passes=("f
                      "rows_per_band": cands[best]["rows_per_band"]}
         del ws
     return out
+
+
+def apply_selection(d, selection: Dict[str, dict]) -> None:
+    """Re-install a selection returned by tune_layer (e.g. loaded from a file) without timing."""
+    for name, r in selection.items():
+        p = PASSES[name]
+        cands = ops.dwconv_plan_candidates(d, p)
+        idx = int(r["index"])
+        if idx >= len(cands):
+            raise RuntimeError(f"plan selection {name}:{idx} out of range ({len(cands)} candidates)")
+        c = cands[idx]
+        if (c["grid"], c["block"]) != (r["grid"], r["block"]):
+            raise RuntimeError(f"plan selection {name}:{idx} no longer matches the candidate list")
+        ops.dwconv_plan_select(d, p, idx)

@@ -20,6 +20,7 @@ ap.add_argument("--dtype", default="f32")
 ap.add_argument("--layout", default="nchw")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--plan", action="store_true")
+ap.add_argument("--plans", default="", help="bench.py --plans file: install this layer's measured selection")
 a = ap.parse_args()
 L = [l for l in synth.mobilenet_v1_dw(a.batch, a.alpha, a.res) if l.name == a.layer][0]
 lay = dwl.NCHW if a.layout == "nchw" else dwl.NHWC
@@ -32,6 +33,11 @@ w = torch.randn(L.c * L.m, L.k, L.k, device="cuda").to(dt)
 y = torch.empty_like(dy)
 dx = torch.empty_like(x)
 dw = torch.empty(L.c * L.m, L.k, L.k, device="cuda")
+if a.plans and os.path.exists(a.plans):
+    import json
+    from paper_1803_09926_b200 import tune
+    with open(a.plans) as f:
+        tune.apply_selection(d, json.load(f).get(a.layer, {}))
 ws = torch.zeros(max(16, ops.dwconv_bwd_filter_workspace_bytes(d)), dtype=torch.uint8, device="cuda")
 if a.plan:
     for p in range(3):

@@ -106,7 +106,7 @@ def main():
         dram = l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0)
         alg = (L.x_elems() + L.y_elems()) * eb + (L.w_elems() * eb if pas != "bwd_filter" else L.w_elems() * 4)
         import re
-        mm = re.search(r"(nchw_\w+_kernel|generic_\w+)<([^>]*)>", l["name"])
+        mm = re.search(r"(nchw_\w+_kernel|nhwc_\w+_kernel|dbf_kernel|generic_\w+)<([^>]*)>", l["name"])
         name = f"{mm.group(1)}<{mm.group(2)}>" if mm else l["name"][:40]
         md.append(f"| {i} | {L.name} | {pas} | {name} | {t_ns / 1e3:.2f} | {100 * t_ns / tot:.1f}% | {dram / 1e6:.1f} | "
                   f"{alg / 1e6:.1f} | {alg / t_ns:.0f} |")
@@ -118,12 +118,16 @@ def main():
     old.update(traffic)
     json.dump(old, open(tpath, "w"), indent=1, sort_keys=True)
 
-    for rep in sorted(glob.glob(os.path.join(a.src, "full_*.ncu-rep"))):
-        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    reps = [(r, os.path.basename(r)[5:-8]) for r in sorted(glob.glob(os.path.join(a.src, "full_*.ncu-rep")))]
+    reps += [(r, os.path.basename(r)[4:-4]) for r in sorted(glob.glob(os.path.join(a.src, "raw_*.csv")))]
+    for rep, tag in reps:
+        if rep.endswith(".csv"):  # raw page exported on the GPU box (ncu -i ... --page raw --csv)
+            out = open(rep).read()
+        else:
+            out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(out.splitlines()))
         h, u, v = rows[0], rows[1], rows[2]
         d = {h[i]: (v[i], u[i]) for i in range(len(h))}
-        tag = os.path.basename(rep)[5:-8]
         md = [f"# ncu --set full: {tag} ({d.get('Kernel Name', ('?',))[0][:120]})", "",
               "| metric | value |", "|---|---|"]
         for k, label in KEYS:
