@@ -250,6 +250,10 @@ def main():
                  dw=bucket.views[len(bufs)],
                  wsb=ops.dwconv_bwd_filter_workspace_bytes(d))
         bufs.append(b)
+    # fused backward (dx + dw in one pass over x and dy) where the library has the kernel
+    for b in bufs:
+        b["fused"] = (args.fused == "all" or (args.fused == "small" and b["L"].h <= 14)) and \
+            ops.dwconv_plan(b["d"], 3)["variant_name"] != "none"
     # measured plan selection (tune.py): time every candidate launch shape of each
     # pass on this layer's tensors and keep the fastest (before any graph capture)
     tuned = {}
@@ -264,7 +268,9 @@ def main():
                 tuned[b["L"].name] = saved[b["L"].name]
                 tune.apply_selection(b["d"], tuned[b["L"].name])
             else:
-                tuned[b["L"].name] = tune.tune_layer(b["d"], b["x"], b["dy"], b["w"])
+                tuned[b["L"].name] = tune.tune_layer(b["d"], b["x"], b["dy"], b["w"],
+                                                     passes=("fwd", "bwd") if b["fused"] else
+                                                     ("fwd", "bwd_data", "bwd_filter"))
             b["wsb"] = ops.dwconv_bwd_filter_workspace_bytes(b["d"])
         torch.cuda.synchronize()
         if args.plans and saved is None and rank == 0:
@@ -282,10 +288,6 @@ def main():
     def launch_bf(b):
         ops.dwconv_bwd_filter(b["d"], b["x"], b["dy"], b["dw"], ws)
 
-    # fused backward (dx + dw in one pass over x and dy) where the library has the kernel
-    for b in bufs:
-        b["fused"] = (args.fused == "all" or (args.fused == "small" and b["L"].h <= 14)) and \
-            ops.dwconv_plan(b["d"], 3)["variant_name"] != "none"
     wsf = torch.zeros(max([16] + [ops.dwconv_bwd_workspace_bytes(b["d"]) for b in bufs if b["fused"]]),
                       dtype=torch.uint8, device=dev)
 

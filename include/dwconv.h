@@ -181,7 +181,8 @@ DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* inf
  * the parity rules of DESIGN.md §5, and a bwd_filter candidate may need a
  * different workspace size (dwconv_bwd_filter_workspace_bytes reflects the
  * selection; re-query after selecting, and zero-fill a new workspace).
- *   dwconv_plan_candidates: pass in {FWD, BWD_DATA, BWD_FILTER}; writes at most
+ *   dwconv_plan_candidates: pass in {FWD, BWD_DATA, BWD_FILTER, BWD (fused backward;
+ *     dwconv_bwd_workspace_bytes reflects its selection)}; writes at most
  *     max_candidates entries to infos (caller-owned array) and the number written
  *     to *count; max_candidates = 0 only reports the total in *count.  Non-NCHW
  *     layouts, N = 0 and the generic override report 0 candidates.

@@ -147,6 +147,12 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
     if ((pass != DWCONV_PASS_BWD_FILTER && pass != DWCONV_PASS_BWD) || p->chunk.max_chain <= 160)
       p->variant = DWCONV_VARIANT_NCHW_CHUNK;
   }
+  // small square planes: the warp-task kernels (nchw_small.cu) when eligible
+  ChunkPlan sp;
+  if (g.layout == DWCONV_NCHW && pass != DWCONV_PASS_BWD && dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &sp)) {
+    p->chunk = sp;
+    p->variant = DWCONV_VARIANT_NCHW_CHUNK;
+  }
   if (pass == DWCONV_PASS_BWD) {  // fused backward: NCHW chunk family, fp32 (bf16 measured slower fused)
     if (p->variant != DWCONV_VARIANT_NCHW_CHUNK || g.dtype != DWCONV_F32) p->variant = DWCONV_VARIANT_NONE;
     return;
@@ -229,7 +235,8 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
   make_plan(g, DWCONV_PASS_FWD, di, &p);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // the NCHW kernels store y with V-wide vector stores straight from registers
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(y) % 16) == 0)
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(y) % 16) == 0 &&
+      (!p.chunk.small || (reinterpret_cast<uintptr_t>(x) % 16) == 0))
     return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
   if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(x, y))
     return cuda_status(dwk::launch_nhwc_tma(g, p.tma, x, w, y, st));
@@ -254,7 +261,8 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
   make_plan(g, DWCONV_PASS_BWD_DATA, di, &p);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // the NCHW kernels store dx with vector stores straight from registers
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0)
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0 &&
+      (!p.chunk.small || (reinterpret_cast<uintptr_t>(dy) % 16) == 0))
     return cuda_status(dwk::launch_nchw_bwd_data(g, p.chunk, dy, w, dx, st));
   if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(dy, dx))
     return cuda_status(dwk::launch_nhwc_tma(g, p.tma, dy, w, dx, st));
@@ -293,8 +301,8 @@ int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float
   Plan p;
   make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
   // the register-direct variant needs 16-B aligned x and dy (vector loads)
-  const bool direct_ok =
-      !p.chunk.direct || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0;
+  const bool direct_ok = !(p.chunk.direct || p.chunk.small) ||
+                         ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0;
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && direct_ok) {
     if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
     if (!workspace) return DWCONV_ERR_NULL_POINTER;
@@ -374,7 +382,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
   int s = validate(d, &g);
   if (s != DWCONV_OK) return s;
   if (!count || (max_candidates > 0 && !infos)) return DWCONV_ERR_NULL_POINTER;
-  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD_FILTER || max_candidates < 0) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD || max_candidates < 0) return DWCONV_ERR_BAD_DESCRIPTOR;
   DevInfo di;
   if ((s = check_device(&di))) return s;
   *count = 0;
@@ -393,6 +401,19 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     if (dp.variant == DWCONV_VARIANT_NCHW_CHUNK) cands.push_back(dp.chunk);
     std::vector<ChunkPlan> more;
     ChunkPlan scratch;
+    if (!cands.empty() && cands[0].small) {
+      // other CTA sizes / ring depths of the small-plane kernel, then the chunk family's own pick
+      static const int shapes[][2] = {{2, 2}, {2, 3}, {4, 2}, {8, 2}, {8, 3}, {8, 4}};
+      for (const auto& sh : shapes) {
+        ChunkPlan v;
+        if (dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1]) &&
+            !(v.threads == cands[0].threads && v.ns == cands[0].ns))
+          cands.push_back(v);
+      }
+      if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch) &&
+          (pass != DWCONV_PASS_BWD_FILTER || scratch.max_chain <= 160))
+        cands.push_back(scratch);
+    }
     if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch, &more, DWCONV_MAX_CANDIDATES) || !more.empty()) {
       for (const ChunkPlan& c : more) {
         if ((int)cands.size() >= DWCONV_MAX_CANDIDATES) break;
@@ -400,7 +421,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         for (const ChunkPlan& o : cands)
           dup = dup || (o.P == c.P && o.nbands == c.nbands && o.band_rows == c.band_rows && o.threads == c.threads &&
                         o.tpg == c.tpg && o.ns == c.ns && o.pair == c.pair && o.direct == c.direct &&
-                        o.nslices == c.nslices && o.grid == c.grid);
+                        o.small == c.small && o.nslices == c.nslices && o.grid == c.grid);
         if (!dup) cands.push_back(c);
       }
     }
@@ -417,7 +438,7 @@ int dwconv_plan_select(const dwconv_desc* d, int pass, int index) {
   Geom g;
   int s = validate(d, &g);
   if (s != DWCONV_OK) return s;
-  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD_FILTER) return DWCONV_ERR_BAD_DESCRIPTOR;
+  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD) return DWCONV_ERR_BAD_DESCRIPTOR;
   DevInfo di;
   if ((s = check_device(&di))) return s;
   const PlanKey key = plan_key(g, pass, di);

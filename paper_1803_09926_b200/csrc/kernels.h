@@ -24,6 +24,20 @@ cudaError_t launch_generic_fwd(const Geom& g, const void* x, const void* w, void
 cudaError_t launch_generic_bwd_data(const Geom& g, const void* dy, const void* w, void* dx, cudaStream_t st);
 cudaError_t launch_generic_bwd_filter(const Geom& g, const void* x, const void* dy, float* dw, cudaStream_t st);
 
+// ---- NCHW small-plane warp-task kernels (W = H in {7,14,28}, 3x3 s1 p1 m1): nchw_small.cu
+struct SmallPlan {
+  int warps, ns, grid, smem;
+  uint32_t slot_bytes;
+  int64_t ntasks;
+  int groups, nslices, nps, max_chain;
+  size_t ws_bytes;
+};
+// warps / stages: CTA size and per-warp ring depth (0 = the defaults, env DWCONV_SMALL_WARPS / _STAGES)
+bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* plan, int warps = 0,
+                     int stages = 0);
+cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const void* in, const void* in2,
+                              const void* w, void* out, float* dw, void* ws, cudaStream_t st);
+
 // ---- NCHW chunk kernels: nchw_chunk.cu
 struct ChunkPlan {
   int threads;          // CTA size
@@ -58,6 +72,9 @@ struct ChunkPlan {
   // bwd_filter register-direct variant (direct_bwd_filter.cu): no smem staging
   bool direct;
   int dL, dSPW, dspc;   // lanes per row set, row sets per warp, row sets per channel
+  // small-plane warp-task kernels (nchw_small.cu)
+  bool small;
+  SmallPlan sp;
 };
 
 constexpr int kPassBwdFused = DWCONV_PASS_BWD;  // plan_nchw pass id of the fused backward
@@ -67,6 +84,8 @@ constexpr int kPassBwdFused = DWCONV_PASS_BWD;  // plan_nchw pass id of the fuse
 // at most max_cands, for measurement-driven selection (dwconv_plan_candidates).
 bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan,
                std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
+bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps = 0,
+                      int stages = 0);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st);
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,

@@ -591,8 +591,32 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   return a;
 }
 
+// A ChunkPlan that runs the small-plane warp-task kernels (nchw_small.cu).
+bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages) {
+  SmallPlan sp;
+  if (!plan_nchw_small(g, pass, num_sms, smem_optin, &sp, warps, stages)) return false;
+  *p = ChunkPlan{};
+  p->small = true;
+  p->sp = sp;
+  p->threads = 32 * sp.warps;
+  p->grid = sp.grid;
+  p->smem_bytes = sp.smem;
+  p->P = 4;
+  p->nbands = 1;
+  p->band_rows = (int)g.H;
+  p->ns = sp.ns;
+  p->nchunks = (pass == DWCONV_PASS_BWD_FILTER) ? (int64_t)sp.groups * sp.nslices : sp.ntasks;
+  p->groups = sp.groups;
+  p->nslices = sp.nslices;
+  p->n_per_slice = sp.nps;
+  p->max_chain = sp.max_chain;
+  p->ws_bytes = sp.ws_bytes;
+  return true;
+}
+
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st) {
+  if (p.small) return launch_nchw_small(g, p.sp, 0, x, nullptr, w, y, nullptr, nullptr, st);
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.w = w; a.out = y;
   a.wbulk = weights_bulk_ok(g, w);
@@ -602,6 +626,7 @@ cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, co
 
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,
                                  cudaStream_t st) {
+  if (p.small) return launch_nchw_small(g, p.sp, 1, dy, nullptr, w, dx, nullptr, nullptr, st);
   nchw::NArgs a = base_args(g, p);
   a.in = dy; a.w = w; a.out = dx;
   a.wbulk = weights_bulk_ok(g, w);
@@ -611,6 +636,7 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
 
 cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
                                    void* ws, cudaStream_t st) {
+  if (p.small) return launch_nchw_small(g, p.sp, 2, x, dy, nullptr, nullptr, dw, ws, st);
   const size_t tk = ((size_t)p.groups * 4 + 15) / 16 * 16;
   if (p.direct) {
     direct::DArgs d{};

@@ -1,0 +1,374 @@
+// nchw_small.cu -- NCHW kernels for small square planes (W = H in {7, 14, 28}),
+// 3x3, pad 1, stride 1, m = 1: the 28x28 / 14x14 / 7x7 MobileNet layers.
+//
+//   fwd       y[n,c,oh,ow] = sum_{i,j} w[c,i,j] * x[n,c,oh-1+i,ow-1+j]      (Eq. 3)
+//   bwd_data  dx = the same stencil over dy with w rotated by 180 degrees   (adjoint at s = 1, reading R9)
+//   bwd_filter dw[c,i,j] = sum_{n,oh,ow} x[n,c,oh-1+i,ow-1+j] * dy[n,c,oh,ow] (Eq. 4 diagonal; R5)
+//
+// The chunk kernels (nchw_fwd.cu ...) spend most of their instructions on
+// per-strip index arithmetic when a plane is only 7-28 wide.  Here the unit of
+// work is a WARP TASK of 4 consecutive planes (one contiguous range of x, and of
+// dy for bwd_filter): lane l of the warp owns plane l / 7 and the V = W / 7
+// columns [V*(l%7), V*(l%7)+V) of it (28 of 32 lanes busy), and walks all W rows
+// with a 3-row sliding window, so a row costs 1 vector LDS + 2 halo LDS and
+// 9*V FFMA.  Every warp is independent: lane 0 bulk-copies the warp's next
+// tasks into a private ring of `ns` shared-memory slots (cp.async.bulk ->
+// UBLKCP, one mbarrier per slot); there is no CTA-wide synchronisation in the
+// loop.  fwd / bwd_data store straight from registers (STG.64/.128 along the
+// row).  bwd_filter: CTA = (group of 4 channels, batch slice), warps split the
+// slice's images; deterministic reduction: rows x V columns per lane (<= 28
+// terms) -> per-image partials added to a running sum (<= 32 images per warp)
+// -> the 7 lanes of a plane in order -> the warps in order -> per-slice partial
+// in the workspace -> last CTA of the group (integer ticket) sums the slices
+// pairwise in slice order and re-zeroes the workspace (as nchw_bwd_filter.cu).
+#include "kernels.h"
+#include "nchw_common.cuh"
+
+namespace dwk {
+namespace small {
+
+using nchw::VecIO;
+
+struct SArgs {
+  const void* in;    // fwd: x, bwd_data: dy, bwd_filter: x
+  const void* in2;   // bwd_filter: dy
+  void* out;         // fwd: y, bwd_data: dx
+  const void* w;
+  float* dw;
+  float* ws_part;
+  unsigned* ws_ticket;
+  int64_t ntasks;    // fwd / bwd_data: Q / 4
+  int C, N;
+  int ns;            // ring slots per warp
+  uint32_t slot_bytes;
+  int groups, nslices, nps;  // bwd_filter
+};
+
+// one row of the window: the lane's V columns and the two halo columns
+template <class T, int W, int V>
+__device__ __forceinline__ void load_row(const T* row, int c0, bool lft, bool rgt, float* xv) {
+  float v[V];
+  VecIO<T, V>::load(row + c0, v);
+#pragma unroll
+  for (int u = 0; u < V; ++u) xv[1 + u] = v[u];
+  xv[0] = lft ? Elem<T>::load(row + c0 - 1) : 0.f;
+  xv[V + 1] = rgt ? Elem<T>::load(row + c0 + V) : 0.f;
+}
+
+// MODE 0 fwd, 1 bwd_data (rotated kernel)
+template <class T, int W, int MODE>
+__global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
+  constexpr int V = W / 7, HW = W * W;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = lane / 7, cg = lane - pl * 7;  // plane within the task, column group
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const T* __restrict__ in = static_cast<const T*>(a.in);
+  T* __restrict__ out = static_cast<T*>(a.out);
+  const T* __restrict__ wt = static_cast<const T*>(a.w);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * nwarps;
+  const uint32_t task_bytes = 4u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int64_t t, int s) {
+    if (lane == 0 && t < a.ntasks) {
+      mbar_arrive_expect_tx(&bars[s], task_bytes);
+      bulk_g2s(slot(s), in + t * 4 * HW, task_bytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = gw; t < a.ntasks; t += stride) {
+    const int64_t q = t * 4 + pl;  // plane
+    const int c = (int)(q % a.C);
+    float wr[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wr[k] = Elem<T>::ldg(wt + (int64_t)c * 9 + (MODE == 1 ? 8 - k : k));
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      const T* pln = slot(s) + pl * HW;
+      const bool lft = c0 > 0, rgt = c0 + V < W;
+      float xw[3][V + 2];
+#pragma unroll
+      for (int u = 0; u < V + 2; ++u) xw[0][u] = 0.f;  // row -1
+      load_row<T, W, V>(pln, c0, lft, rgt, xw[1]);
+      T* po = out + q * HW + c0;
+#pragma unroll
+      for (int r = 0; r < W; ++r) {
+        if (r + 1 < W) load_row<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
+        else
+#pragma unroll
+          for (int u = 0; u < V + 2; ++u) xw[2][u] = 0.f;  // row W
+        float o[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          float acc = wr[0] * xw[0][u];
+#pragma unroll
+          for (int k = 1; k < 9; ++k) acc = fmaf(wr[k], xw[k / 3][u + k % 3], acc);
+          o[u] = acc;
+        }
+        VecIO<T, V>::store(po + r * W, o);
+#pragma unroll
+        for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
+      }
+    }
+    __syncwarp();
+    issue(t + a.ns * stride, s);  // the slot is free: every lane is past it
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  griddep_launch_dependents();
+}
+
+template <class T, int W>
+__global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
+  constexpr int V = W / 7, HW = W * W;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = lane / 7, cg = lane - pl * 7;
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
+  const int cb = g * 4;  // first channel of the group
+  const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const uint32_t task_bytes = 4u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int n, int s) {
+    if (lane == 0 && n < n1) {
+      const int64_t off = ((int64_t)n * a.C + cb) * HW;
+      mbar_arrive_expect_tx(&bars[s], 2 * task_bytes);
+      bulk_g2s(slot(s), x + off, task_bytes, &bars[s]);
+      bulk_g2s(slot(s) + 4 * HW, dy + off, task_bytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
+  float run[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) run[k] = 0.f;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int n = n0 + warp; n < n1; n += nwarps) {
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      const T* pln = slot(s) + pl * HW;
+      const T* pd = slot(s) + 4 * HW + pl * HW;
+      const bool lft = c0 > 0, rgt = c0 + V < W;
+      float xw[3][V + 2];
+#pragma unroll
+      for (int u = 0; u < V + 2; ++u) xw[0][u] = 0.f;
+      load_row<T, W, V>(pln, c0, lft, rgt, xw[1]);
+      float loc[9];
+#pragma unroll
+      for (int r = 0; r < W; ++r) {
+        if (r + 1 < W) load_row<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
+        else
+#pragma unroll
+          for (int u = 0; u < V + 2; ++u) xw[2][u] = 0.f;
+        float d[V];
+        VecIO<T, V>::load(pd + r * W + c0, d);
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+#pragma unroll
+          for (int u = 0; u < V; ++u)
+            loc[k] = (r == 0 && u == 0) ? xw[k / 3][u + k % 3] * d[u] : fmaf(xw[k / 3][u + k % 3], d[u], loc[k]);
+#pragma unroll
+        for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) run[k] += loc[k];
+    }
+    __syncwarp();
+    issue(n + a.ns * nwarps, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  griddep_launch_dependents();
+  // ---- lanes of a plane in order, then warps in order -> the slice partial
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem + 64 * nwarps);  // [warp][lane][9]; the ring is idle now
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) red[(warp * 32 + lane) * 9 + k] = run[k];
+  }
+  __syncthreads();
+  float* part = a.ws_part + (int64_t)sl * a.C * 9;
+  for (int e = threadIdx.x; e < 4 * 9; e += blockDim.x) {
+    const int p = e / 9, k = e - p * 9;
+    float tot = 0.f;
+    for (int wv = 0; wv < nwarps; ++wv) {
+      float v = red[(wv * 32 + p * 7) * 9 + k];
+      for (int l = 1; l < 7; ++l) v += red[(wv * 32 + p * 7 + l) * 9 + k];
+      tot = (wv == 0) ? v : tot + v;
+    }
+    part[(int64_t)(cb + p) * 9 + k] = tot;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
+    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int64_t e0 = (int64_t)cb * 9;
+    const int64_t sstride = (int64_t)a.C * 9;
+    for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) {
+      float stk[16];
+      int top = 0;
+      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
+        float vals[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int s2 = s0 + u;
+          if (s2 < a.nslices) {
+            float cur = vals[u];
+            int bits = s2;
+            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+            stk[top++] = cur;
+          }
+        }
+      }
+      float tot = stk[--top];
+      while (top > 0) tot = stk[--top] + tot;
+      a.dw[e0 + idx] = tot;
+    }
+    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  }
+}
+
+using SKernelFn = void (*)(SArgs);
+
+template <class T>
+SKernelFn pick(int pass, int W) {
+  switch (W) {
+    case 7: return pass == 0 ? small_fd_kernel<T, 7, 0> : pass == 1 ? small_fd_kernel<T, 7, 1> : small_bf_kernel<T, 7>;
+    case 14: return pass == 0 ? small_fd_kernel<T, 14, 0> : pass == 1 ? small_fd_kernel<T, 14, 1> : small_bf_kernel<T, 14>;
+    case 28: return pass == 0 ? small_fd_kernel<T, 28, 0> : pass == 1 ? small_fd_kernel<T, 28, 1> : small_bf_kernel<T, 28>;
+    default: return nullptr;
+  }
+}
+SKernelFn kernel_for(int dtype, int pass, int W) {
+  return dtype == DWCONV_F32 ? pick<float>(pass, W) : pick<__nv_bfloat16>(pass, W);
+}
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  return (v >= lo && v <= hi) ? v : dflt;
+}
+
+}  // namespace small
+
+// Eligibility + launch shape.  pass: 0 fwd, 1 bwd_data, 2 bwd_filter.
+bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages) {
+  using namespace small;
+  static const int on = env_int("DWCONV_SMALL", 1, 0, 1);
+  if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
+  if (g.sh != 1 || g.sw != 1 || g.H != g.W || (g.W != 7 && g.W != 14 && g.W != 28)) return false;
+  if (g.C % 4 != 0 || g.N < 1) return false;
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  const int64_t task_bytes = 4 * g.H * g.W * eb;
+  if (task_bytes % 16 != 0) return false;  // bulk copies: 16-B granules (bf16 7x7 takes the chunk kernels)
+  *p = SmallPlan{};
+  static const int warps_env = env_int("DWCONV_SMALL_WARPS", 4, 1, 8);
+  static const int ns_env = env_int("DWCONV_SMALL_STAGES", 3, 2, 6);
+  p->warps = warps > 0 ? warps : warps_env;
+  p->ns = stages > 0 ? stages : ns_env;
+  p->slot_bytes = (uint32_t)((pass == 2 ? 2 : 1) * task_bytes);
+  p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
+  if (pass == 2) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * 9 * 4);
+  if (p->smem > smem_optin - 1024) return false;
+  SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W);
+  if (!fn) return false;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - (int)fa.sharedSizeBytes) !=
+      cudaSuccess)
+    return false;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * p->warps, p->smem) != cudaSuccess || occ < 1)
+    return false;
+  if (pass != 2) {
+    p->ntasks = g.N * g.C / 4;
+    p->grid = (int)std::min<int64_t>((p->ntasks + p->warps - 1) / p->warps, (int64_t)occ * num_sms);
+    p->max_chain = 9;
+    return true;
+  }
+  // bwd_filter: groups of 4 channels x batch slices, ~one wave, <= 32 images per warp
+  p->groups = (int)(g.C / 4);
+  int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
+  nsl = std::max<int64_t>(nsl, (g.N + 32 * p->warps - 1) / (32 * p->warps));
+  nsl = std::min<int64_t>(nsl, std::min<int64_t>(g.N, 128));
+  int64_t nps = (g.N + nsl - 1) / nsl;
+  nsl = (g.N + nps - 1) / nps;
+  p->nslices = (int)nsl;
+  p->nps = (int)nps;
+  p->grid = (int)(p->groups * nsl);
+  const int64_t per_warp = (nps + p->warps - 1) / p->warps;
+  int ls = 0;
+  while ((1ll << ls) < nsl) ++ls;
+  p->max_chain = (int)(g.W * (g.W / 7) + per_warp + 7 + p->warps + 2 * ls + 1);
+  const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
+  p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
+  return p->max_chain <= 160;
+}
+
+cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const void* in, const void* in2,
+                              const void* w, void* out, float* dw, void* ws, cudaStream_t st) {
+  using namespace small;
+  SArgs a{};
+  a.in = in; a.in2 = in2; a.out = out; a.w = w; a.dw = dw;
+  a.ntasks = p.ntasks;
+  a.C = (int)g.C; a.N = (int)g.N;
+  a.ns = p.ns; a.slot_bytes = p.slot_bytes;
+  a.groups = p.groups; a.nslices = p.nslices; a.nps = p.nps;
+  if (pass == 2) {
+    const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
+    a.ws_ticket = static_cast<unsigned*>(ws);
+    a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
+  }
+  SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W);
+  if (!fn) return cudaErrorInvalidValue;
+  static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.grid);
+  cfg.blockDim = dim3((unsigned)(32 * p.warps));
+  cfg.dynamicSmemBytes = (size_t)p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+}  // namespace dwk

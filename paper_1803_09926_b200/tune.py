@@ -21,9 +21,9 @@ from typing import Dict, List, Optional
 import torch
 
 from . import ops
-from ._lib import NCHW, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_FWD
+from ._lib import NCHW, PASS_BWD, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_FWD
 
-PASSES = {"fwd": PASS_FWD, "bwd_data": PASS_BWD_DATA, "bwd_filter": PASS_BWD_FILTER}
+PASSES = {"fwd": PASS_FWD, "bwd_data": PASS_BWD_DATA, "bwd_filter": PASS_BWD_FILTER, "bwd": PASS_BWD}
 
 
 def _graph_us(calls, reps: int, stream: torch.cuda.Stream) -> float:
@@ -73,7 +73,7 @@ def tune_layer(d, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, passes=("f
         if len(cands) <= 1:
             continue
         ws = None
-        if p == PASS_BWD_FILTER:
+        if p in (PASS_BWD_FILTER, PASS_BWD):
             ws = torch.zeros(max(16, max(c["workspace_bytes"] for c in cands)), dtype=torch.uint8, device=dev)
 
         def mk(s):
@@ -81,6 +81,8 @@ def tune_layer(d, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, passes=("f
                 return lambda: ops.dwconv_fwd(d, s["x"], w, s["y"])
             if p == PASS_BWD_DATA:
                 return lambda: ops.dwconv_bwd_data(d, s["dy"], w, s["dx"])
+            if p == PASS_BWD:
+                return lambda: ops.dwconv_bwd(d, s["x"], s["dy"], w, s["dx"], dw, ws)
             return lambda: ops.dwconv_bwd_filter(d, s["x"], s["dy"], dw, ws)
 
         times = []

@@ -82,6 +82,24 @@ def _check_layer(L, dtype, amax, seed):
                         assert np.array_equal(got[c], r.astype(np.float32)), tag
         finally:
             ops.dwconv_plan_select(d, pas, -1)
+    # fused backward (dwconv_bwd: dx and dw from one pass) where the library has it
+    if ops.dwconv_plan(d, 3)["variant_name"] != "none":
+        cands = ops.dwconv_plan_candidates(d, 3)
+        ws = torch.zeros(max(16, max(c["workspace_bytes"] for c in cands)), dtype=torch.uint8, device="cuda")
+        try:
+            for i, cand in enumerate(cands):
+                ops.dwconv_plan_select(d, 3, i)
+                tag = f"{L.name} {dtype} bwd (fused) candidate {i} {cand}"
+                dx.fill_(float("nan"))
+                dwt.fill_(float("nan"))
+                ops.dwconv_bwd(d, xd, dyd, wd, dx, dwt, ws)
+                for (n, c), r in ref["bwd_data"].items():
+                    assert np.array_equal(dx[n, c].float().cpu().numpy(), r.astype(np.float32)), tag
+                got = dwt.cpu().numpy()
+                for c, r in ref["bwd_filter"].items():
+                    assert np.array_equal(got[c], r.astype(np.float32)), tag
+        finally:
+            ops.dwconv_plan_select(d, 3, -1)
     torch.cuda.synchronize()
 
 
