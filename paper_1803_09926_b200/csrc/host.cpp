@@ -149,7 +149,8 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
   }
   // small square planes: the warp-task kernels (nchw_small.cu) when eligible
   ChunkPlan sp;
-  if (g.layout == DWCONV_NCHW && pass != DWCONV_PASS_BWD && dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &sp)) {
+  if (g.layout == DWCONV_NCHW && (pass != DWCONV_PASS_BWD || g.dtype == DWCONV_F32) &&
+      dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &sp)) {
     p->chunk = sp;
     p->variant = DWCONV_VARIANT_NCHW_CHUNK;
   }
@@ -351,7 +352,8 @@ int dwconv_bwd(const dwconv_desc* d, const void* x, const void* dy, const void* 
   Plan p;
   if (g.N > 0) make_plan(g, DWCONV_PASS_BWD, di, &p);
   // the fused kernel stores dx with vector stores straight from registers
-  if (g.N > 0 && p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0) {
+  if (g.N > 0 && p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0 &&
+      (!p.chunk.small || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0)) {
     if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
     if (!workspace) return DWCONV_ERR_NULL_POINTER;
     if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
@@ -403,15 +405,19 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     ChunkPlan scratch;
     if (!cands.empty() && cands[0].small) {
       // other CTA sizes / ring depths of the small-plane kernel, then the chunk family's own pick
-      static const int shapes[][2] = {{2, 2}, {2, 3}, {4, 2}, {8, 2}, {8, 3}, {8, 4}};
+      // {warps, ring slots, batch slices (bwd_filter; 0 = about one wave)}
+      static const int shapes[][3] = {{2, 2, 0}, {2, 3, 0}, {4, 2, 0}, {8, 2, 0}, {8, 3, 0}, {8, 4, 0},
+                                      {8, 2, 1}, {8, 3, 1}, {8, 2, 2}, {4, 3, 2}};
       for (const auto& sh : shapes) {
+        if (sh[2] && pass < DWCONV_PASS_BWD_FILTER) continue;
         ChunkPlan v;
-        if (dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1]) &&
-            !(v.threads == cands[0].threads && v.ns == cands[0].ns))
-          cands.push_back(v);
+        if (!dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2])) continue;
+        bool dup = false;
+        for (const ChunkPlan& o : cands) dup = dup || (o.small && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices);
+        if (!dup) cands.push_back(v);
       }
       if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch) &&
-          (pass != DWCONV_PASS_BWD_FILTER || scratch.max_chain <= 160))
+          (pass < DWCONV_PASS_BWD_FILTER || scratch.max_chain <= 160))
         cands.push_back(scratch);
     }
     if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch, &more, DWCONV_MAX_CANDIDATES) || !more.empty()) {

@@ -33,8 +33,9 @@ struct SmallPlan {
   size_t ws_bytes;
 };
 // warps / stages: CTA size and per-warp ring depth (0 = the defaults, env DWCONV_SMALL_WARPS / _STAGES)
+// slices (bwd_filter): batch slices per channel group (0 = about one wave of CTAs)
 bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* plan, int warps = 0,
-                     int stages = 0);
+                     int stages = 0, int slices = 0);
 cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const void* in, const void* in2,
                               const void* w, void* out, float* dw, void* ws, cudaStream_t st);
 
@@ -85,7 +86,7 @@ constexpr int kPassBwdFused = DWCONV_PASS_BWD;  // plan_nchw pass id of the fuse
 bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan,
                std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
 bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps = 0,
-                      int stages = 0);
+                      int stages = 0, int slices = 0);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st);
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,

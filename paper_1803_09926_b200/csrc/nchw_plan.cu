@@ -592,9 +592,10 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
 }
 
 // A ChunkPlan that runs the small-plane warp-task kernels (nchw_small.cu).
-bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages) {
+bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages,
+                      int slices) {
   SmallPlan sp;
-  if (!plan_nchw_small(g, pass, num_sms, smem_optin, &sp, warps, stages)) return false;
+  if (!plan_nchw_small(g, pass, num_sms, smem_optin, &sp, warps, stages, slices)) return false;
   *p = ChunkPlan{};
   p->small = true;
   p->sp = sp;
@@ -605,7 +606,7 @@ bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, Chun
   p->nbands = 1;
   p->band_rows = (int)g.H;
   p->ns = sp.ns;
-  p->nchunks = (pass == DWCONV_PASS_BWD_FILTER) ? (int64_t)sp.groups * sp.nslices : sp.ntasks;
+  p->nchunks = (pass >= DWCONV_PASS_BWD_FILTER) ? (int64_t)sp.groups * sp.nslices : sp.ntasks;
   p->groups = sp.groups;
   p->nslices = sp.nslices;
   p->n_per_slice = sp.nps;
@@ -676,6 +677,7 @@ cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void
 
 cudaError_t launch_nchw_bwd_fused(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, const void* w,
                                   void* dx, float* dw, void* ws, cudaStream_t st) {
+  if (p.small) return launch_nchw_small(g, p.sp, 3, x, dy, w, dx, dw, ws, st);
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.in2 = dy; a.dw = dw; a.w = w; a.out = dx;
   const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;

@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
   griddep_launch_dependents();
 }
 
-template <class T, int W>
+// FUSED: also dx = the forward stencil over the staged dy with the rotated kernel
+// (the fused backward): x and dy leave HBM once for both gradients.
+template <class T, int W, bool FUSED = false>
 __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
   constexpr int V = W / 7, HW = W * W;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -164,6 +166,13 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
+  float wf[FUSED ? 9 : 1];  // rotated kernel of this lane's channel (fused dx)
+  if constexpr (FUSED) {
+    const T* __restrict__ wt = static_cast<const T*>(a.w);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wf[k] = Elem<T>::ldg(wt + (int64_t)(cb + (live ? pl : 0)) * 9 + 8 - k);
+  }
+  T* __restrict__ dxo = static_cast<T*>(a.out);
   float run[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) run[k] = 0.f;
@@ -180,6 +189,13 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
       for (int u = 0; u < V + 2; ++u) xw[0][u] = 0.f;
       load_row<T, W, V>(pln, c0, lft, rgt, xw[1]);
       float loc[9];
+      float dw3[FUSED ? 3 : 1][V + 2];  // dy window (fused dx)
+      T* po = dxo + ((int64_t)n * a.C + cb + pl) * HW + c0;
+      if constexpr (FUSED) {
+#pragma unroll
+        for (int u = 0; u < V + 2; ++u) dw3[0][u] = 0.f;
+        load_row<T, W, V>(pd, c0, lft, rgt, dw3[1]);
+      }
 #pragma unroll
       for (int r = 0; r < W; ++r) {
         if (r + 1 < W) load_row<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
@@ -187,7 +203,26 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
 #pragma unroll
           for (int u = 0; u < V + 2; ++u) xw[2][u] = 0.f;
         float d[V];
-        VecIO<T, V>::load(pd + r * W + c0, d);
+        if constexpr (FUSED) {
+          if (r + 1 < W) load_row<T, W, V>(pd + (r + 1) * W, c0, lft, rgt, dw3[2]);
+          else
+#pragma unroll
+            for (int u = 0; u < V + 2; ++u) dw3[2][u] = 0.f;
+          float o[V];
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            d[u] = dw3[1][u + 1];
+            float acc = wf[0] * dw3[0][u];
+#pragma unroll
+            for (int k = 1; k < 9; ++k) acc = fmaf(wf[k], dw3[k / 3][u + k % 3], acc);
+            o[u] = acc;
+          }
+          VecIO<T, V>::store(po + r * W, o);
+#pragma unroll
+          for (int u = 0; u < V + 2; ++u) { dw3[0][u] = dw3[1][u]; dw3[1][u] = dw3[2][u]; }
+        } else {
+          VecIO<T, V>::load(pd + r * W + c0, d);
+        }
 #pragma unroll
         for (int k = 0; k < 9; ++k)
 #pragma unroll
@@ -269,9 +304,12 @@ using SKernelFn = void (*)(SArgs);
 template <class T>
 SKernelFn pick(int pass, int W) {
   switch (W) {
-    case 7: return pass == 0 ? small_fd_kernel<T, 7, 0> : pass == 1 ? small_fd_kernel<T, 7, 1> : small_bf_kernel<T, 7>;
-    case 14: return pass == 0 ? small_fd_kernel<T, 14, 0> : pass == 1 ? small_fd_kernel<T, 14, 1> : small_bf_kernel<T, 14>;
-    case 28: return pass == 0 ? small_fd_kernel<T, 28, 0> : pass == 1 ? small_fd_kernel<T, 28, 1> : small_bf_kernel<T, 28>;
+    case 7: return pass == 0 ? small_fd_kernel<T, 7, 0> : pass == 1 ? small_fd_kernel<T, 7, 1>
+                 : pass == 2 ? small_bf_kernel<T, 7> : small_bf_kernel<T, 7, true>;
+    case 14: return pass == 0 ? small_fd_kernel<T, 14, 0> : pass == 1 ? small_fd_kernel<T, 14, 1>
+                  : pass == 2 ? small_bf_kernel<T, 14> : small_bf_kernel<T, 14, true>;
+    case 28: return pass == 0 ? small_fd_kernel<T, 28, 0> : pass == 1 ? small_fd_kernel<T, 28, 1>
+                  : pass == 2 ? small_bf_kernel<T, 28> : small_bf_kernel<T, 28, true>;
     default: return nullptr;
   }
 }
@@ -288,7 +326,8 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 }  // namespace small
 
 // Eligibility + launch shape.  pass: 0 fwd, 1 bwd_data, 2 bwd_filter.
-bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages) {
+bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages,
+                     int slices) {
   using namespace small;
   static const int on = env_int("DWCONV_SMALL", 1, 0, 1);
   if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
@@ -302,9 +341,10 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   static const int ns_env = env_int("DWCONV_SMALL_STAGES", 3, 2, 6);
   p->warps = warps > 0 ? warps : warps_env;
   p->ns = stages > 0 ? stages : ns_env;
-  p->slot_bytes = (uint32_t)((pass == 2 ? 2 : 1) * task_bytes);
+  const bool bf = pass >= 2;  // bwd_filter or the fused backward
+  p->slot_bytes = (uint32_t)((bf ? 2 : 1) * task_bytes);
   p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
-  if (pass == 2) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * 9 * 4);
+  if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * 9 * 4);
   if (p->smem > smem_optin - 1024) return false;
   SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W);
   if (!fn) return false;
@@ -316,7 +356,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * p->warps, p->smem) != cudaSuccess || occ < 1)
     return false;
-  if (pass != 2) {
+  if (!bf) {
     p->ntasks = g.N * g.C / 4;
     p->grid = (int)std::min<int64_t>((p->ntasks + p->warps - 1) / p->warps, (int64_t)occ * num_sms);
     p->max_chain = 9;
@@ -327,6 +367,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
   nsl = std::max<int64_t>(nsl, (g.N + 32 * p->warps - 1) / (32 * p->warps));
   nsl = std::min<int64_t>(nsl, std::min<int64_t>(g.N, 128));
+  if (slices > 0) nsl = std::max<int64_t>(std::min<int64_t>(slices, g.N), (g.N + 32 * p->warps - 1) / (32 * p->warps));
   int64_t nps = (g.N + nsl - 1) / nsl;
   nsl = (g.N + nps - 1) / nps;
   p->nslices = (int)nsl;
@@ -350,7 +391,7 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
   a.C = (int)g.C; a.N = (int)g.N;
   a.ns = p.ns; a.slot_bytes = p.slot_bytes;
   a.groups = p.groups; a.nslices = p.nslices; a.nps = p.nps;
-  if (pass == 2) {
+  if (pass >= 2) {
     const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
