@@ -31,7 +31,11 @@ struct SmallPlan {
   int64_t ntasks;
   int groups, nslices, nps, max_chain;
   size_t ws_bytes;
+  // band bwd_filter for large planes (band_bf_kernel)
+  bool band;
+  int R, V, nbands, cpg;
 };
+bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* plan, int warps, int stages, int rows);
 // warps / stages: CTA size and per-warp ring depth (0 = the defaults, env DWCONV_SMALL_WARPS / _STAGES)
 // slices (bwd_filter): batch slices per channel group (0 = about one wave of CTAs)
 bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* plan, int warps = 0,
@@ -87,6 +91,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
                std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
 bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps = 0,
                       int stages = 0, int slices = 0);
+bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* plan, int warps, int stages, int rows);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st);
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,

@@ -615,6 +615,28 @@ bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, Chun
   return true;
 }
 
+bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages, int rows) {
+  SmallPlan sp;
+  if (!plan_nchw_band_bf(g, num_sms, smem_optin, &sp, warps, stages, rows)) return false;
+  *p = ChunkPlan{};
+  p->small = true;
+  p->sp = sp;
+  p->threads = 32 * sp.warps;
+  p->grid = sp.grid;
+  p->smem_bytes = sp.smem;
+  p->P = 1;
+  p->nbands = sp.nbands;
+  p->band_rows = sp.R;
+  p->ns = sp.ns;
+  p->nchunks = (int64_t)sp.groups * sp.nslices;
+  p->groups = sp.groups;
+  p->nslices = sp.nslices;
+  p->n_per_slice = sp.nps;
+  p->max_chain = sp.max_chain;
+  p->ws_bytes = sp.ws_bytes;
+  return true;
+}
+
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st) {
   if (p.small) return launch_nchw_small(g, p.sp, 0, x, nullptr, w, y, nullptr, nullptr, st);

@@ -42,6 +42,8 @@ struct SArgs {
   int ns;            // ring slots per warp
   uint32_t slot_bytes;
   int groups, nslices, nps;  // bwd_filter
+  // band bwd_filter (band_bf_kernel)
+  int H, W, Ho, Wo, nbands, cpg;  // cpg: channels per group (one per warp)
 };
 
 // one row of the window: the lane's V columns and the two halo columns
@@ -299,7 +301,197 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
   }
 }
 
+// ------------------------------------------------------------ band bwd_filter
+// Large planes (output width Wo = 28 V, V in {1,2,4}; the 112/56/28 MobileNet
+// layers at stride 1 and 2): warp task = (image, band of R dy rows) of ONE
+// channel -- x rows [R*b*S - 1, (R*b + R - 1)*S + 1] and the R dy rows are two
+// contiguous ranges, bulk-copied by lane 0 into the warp's ring slot.  Lane l
+// (< 28) owns dy columns [V*l, V*l + V) and walks the band's rows with a sliding
+// x window (stride 1: one new x row per dy row, stride 2: two), 9*V FFMA per
+// dy row.  CTA = (group of `cpg` channels, one per warp; batch slice).
+// Deterministic reduction: R*V terms per task -> running sum over the warp's
+// tasks -> xor-shuffle tree over the 32 lanes -> per-slice partial -> ticketed
+// pairwise finalize over slices (as above).
+template <class T, int S, int V, int R>
+__global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
+  constexpr int NX = S * V;  // own x columns per lane (stride 2: + the left halo only)
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
+  const int c = g * a.cpg + warp;  // this warp's channel
+  const bool wlive = warp < a.cpg && c < a.C;
+  const bool live = wlive && lane < 28;
+  const int H = a.H, W = a.W, Ho = a.Ho, Wo = a.Wo;
+  const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
+  const int ntask = (n1 - n0) * a.nbands;
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  const uint32_t xcap = (uint32_t)(((R - 1) * S + 3) * W * sizeof(T) + 15) & ~15u;  // x part of a slot
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  auto slot = [&](int s) { return reinterpret_cast<unsigned char*>(ring) + (size_t)s * a.slot_bytes; };
+  auto rows_of = [&](int t, int* n, int* r0, int* r1, int* lo, int* hi) {
+    const int nn = t / a.nbands, b = t - nn * a.nbands;
+    *n = n0 + nn;
+    *r0 = b * R;
+    *r1 = min(*r0 + R, Ho);
+    *lo = max(0, *r0 * S - 1);
+    *hi = min(H, (*r1 - 1) * S + 2);
+  };
+  auto issue = [&](int t, int s) {
+    if (lane == 0 && wlive && t < ntask) {
+      int n, r0, r1, lo, hi;
+      rows_of(t, &n, &r0, &r1, &lo, &hi);
+      const uint32_t xb = (uint32_t)((hi - lo) * W * sizeof(T)), db = (uint32_t)((r1 - r0) * Wo * sizeof(T));
+      mbar_arrive_expect_tx(&bars[s], xb + db);
+      bulk_g2s(slot(s), x + (((int64_t)n * a.C + c) * H + lo) * W, xb, &bars[s]);
+      bulk_g2s(slot(s) + xcap, dy + (((int64_t)n * a.C + c) * Ho + r0) * Wo, db, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(i, i);
+  const int c0 = lane * V;
+  float run[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) run[k] = 0.f;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int t = 0; t < (wlive ? ntask : 0); ++t) {
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      int n, r0, r1, lo, hi;
+      rows_of(t, &n, &r0, &r1, &lo, &hi);
+      const T* xs = reinterpret_cast<const T*>(slot(s)) - (int64_t)lo * W;  // x row ih at xs + ih*W (ih in [lo,hi))
+      const T* ds = reinterpret_cast<const T*>(slot(s) + xcap) - (int64_t)r0 * Wo;
+      // window rows: x row ih = r*S - 1 + i, i = 0..2; columns S*c0 - 1 .. S*c0 + NX (+1 at S = 1)
+      float xw[3][NX + 2];
+      auto ldx = [&](int ih, float* v) {
+        if (ih >= lo && ih < hi) {
+          const T* row = xs + (int64_t)ih * W;
+          float o[NX];
+          VecIO<T, NX>::load(row + S * c0, o);
+#pragma unroll
+          for (int u = 0; u < NX; ++u) v[1 + u] = o[u];
+          v[0] = (c0 > 0) ? Elem<T>::load(row + S * c0 - 1) : 0.f;
+          v[NX + 1] = (S == 1 && c0 + V < W) ? Elem<T>::load(row + c0 + V) : 0.f;
+        } else {
+#pragma unroll
+          for (int u = 0; u < NX + 2; ++u) v[u] = 0.f;
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < 3 - S; ++i) ldx(r0 * S - 1 + i, xw[i]);
+      float loc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) loc[k] = 0.f;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const int r = r0 + rr;
+        if (r < r1) {
+#pragma unroll
+          for (int i = 3 - S; i < 3; ++i) ldx(r * S - 1 + i, xw[i]);
+          float d[V];
+          VecIO<T, V>::load(ds + (int64_t)r * Wo + c0, d);
+#pragma unroll
+          for (int k = 0; k < 9; ++k)
+#pragma unroll
+            for (int u = 0; u < V; ++u) loc[k] = fmaf(xw[k / 3][S * u + k % 3], d[u], loc[k]);
+#pragma unroll
+          for (int i = 0; i < 3 - S; ++i)
+#pragma unroll
+            for (int u = 0; u < NX + 2; ++u) xw[i][u] = xw[i + S][u];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) run[k] += loc[k];
+    }
+    __syncwarp();
+    issue(t + a.ns, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  griddep_launch_dependents();
+  // ---- lanes: fixed xor tree (lanes >= 28 hold zeros) -> the warp's channel partial
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) run[k] += __shfl_xor_sync(0xffffffffu, run[k], off);
+  }
+  float* part = a.ws_part + (int64_t)sl * a.C * 9;
+  if (wlive && lane < 9) {
+    float v = run[0];
+#pragma unroll
+    for (int k = 1; k < 9; ++k) v = (lane == k) ? run[k] : v;
+    part[(int64_t)c * 9 + lane] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
+    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int64_t e0 = (int64_t)g * a.cpg * 9;
+    const int nvals = min(a.cpg, a.C - g * a.cpg) * 9;
+    const int64_t sstride = (int64_t)a.C * 9;
+    for (int idx = threadIdx.x; idx < nvals; idx += blockDim.x) {
+      float stk[16];
+      int top = 0;
+      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
+        float vals[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int s2 = s0 + u;
+          if (s2 < a.nslices) {
+            float cur = vals[u];
+            int bits = s2;
+            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+            stk[top++] = cur;
+          }
+        }
+      }
+      float tot = stk[--top];
+      while (top > 0) tot = stk[--top] + tot;
+      a.dw[e0 + idx] = tot;
+    }
+    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  }
+}
+
 using SKernelFn = void (*)(SArgs);
+
+template <class T, int S, int R>
+SKernelFn band_pick_v(int V) {
+  switch (V) {
+    case 1: return band_bf_kernel<T, S, 1, R>;
+    case 2: return band_bf_kernel<T, S, 2, R>;
+    case 4: return (S == 1 || sizeof(T) == 2) ? band_bf_kernel<T, S, 4, R> : nullptr;
+    default: return nullptr;
+  }
+}
+SKernelFn band_kernel_for(int dtype, int S, int V, int R) {
+  if (dtype == DWCONV_F32) {
+    if (S == 1) return R == 7 ? band_pick_v<float, 1, 7>(V) : band_pick_v<float, 1, 14>(V);
+    return R == 7 ? band_pick_v<float, 2, 7>(V) : band_pick_v<float, 2, 14>(V);
+  }
+  using B = __nv_bfloat16;
+  if (S == 1) return R == 7 ? band_pick_v<B, 1, 7>(V) : band_pick_v<B, 1, 14>(V);
+  return R == 7 ? band_pick_v<B, 2, 7>(V) : band_pick_v<B, 2, 14>(V);
+}
 
 template <class T>
 SKernelFn pick(int pass, int W) {
@@ -382,10 +574,64 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   return p->max_chain <= 160;
 }
 
+// Band bwd_filter for large planes (band_bf_kernel): Wo = 28 V, V in {1, 2, 4}.
+bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages, int rows) {
+  using namespace small;
+  static const int on = env_int("DWCONV_BAND_BF", 1, 0, 1);
+  if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
+  const int S = g.sh;
+  if (g.sw != S || (S != 1 && S != 2) || g.Wo % 28 != 0 || g.W != S * g.Wo || g.N < 1) return false;
+  const int V = (int)(g.Wo / 28);
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  if ((g.W * eb) % 16 != 0 || (g.Wo * eb) % 16 != 0 || g.N * g.C >= ((int64_t)1 << 31)) return false;
+  if (rows != 7 && rows != 14) return false;
+  SKernelFn fn = band_kernel_for(g.dtype, S, V, rows);
+  if (!fn) return false;
+  *p = SmallPlan{};
+  p->band = true;
+  p->R = rows;
+  p->V = V;
+  p->warps = warps;
+  p->ns = stages;
+  const int64_t xcap = ((((int64_t)rows - 1) * S + 3) * g.W * eb + 15) & ~(int64_t)15;
+  p->slot_bytes = (uint32_t)(xcap + (((int64_t)rows * g.Wo * eb + 15) & ~(int64_t)15));
+  p->smem = 64 * warps + warps * stages * (int)p->slot_bytes;
+  if (p->smem > smem_optin - 1024) return false;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - (int)fa.sharedSizeBytes) !=
+      cudaSuccess)
+    return false;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * warps, p->smem) != cudaSuccess || occ < 1)
+    return false;
+  p->nbands = (int)((g.Ho + rows - 1) / rows);
+  p->cpg = warps;
+  p->groups = (int)((g.C + warps - 1) / warps);
+  // slices: about one wave, <= 64 tasks (image x band) per warp, <= 128 slices
+  int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
+  nsl = std::max<int64_t>(nsl, (g.N * p->nbands + 63) / 64);
+  nsl = std::min<int64_t>(nsl, std::min<int64_t>(g.N, 128));
+  int64_t nps = (g.N + nsl - 1) / nsl;
+  nsl = (g.N + nps - 1) / nps;
+  if (nps * p->nbands > 64) return false;
+  p->nslices = (int)nsl;
+  p->nps = (int)nps;
+  p->grid = (int)(p->groups * nsl);
+  int ls = 0;
+  while ((1ll << ls) < nsl) ++ls;
+  p->max_chain = (int)(rows * V + nps * p->nbands + 5 + 2 * ls + 1);
+  const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
+  p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
+  return p->max_chain <= 160;
+}
+
 cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const void* in, const void* in2,
                               const void* w, void* out, float* dw, void* ws, cudaStream_t st) {
   using namespace small;
   SArgs a{};
+  a.H = (int)g.H; a.W = (int)g.W; a.Ho = (int)g.Ho; a.Wo = (int)g.Wo;
+  a.nbands = p.nbands; a.cpg = p.cpg;
   a.in = in; a.in2 = in2; a.out = out; a.w = w; a.dw = dw;
   a.ntasks = p.ntasks;
   a.C = (int)g.C; a.N = (int)g.N;
@@ -396,7 +642,7 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   }
-  SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W);
+  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R) : kernel_for(g.dtype, pass, (int)g.W);
   if (!fn) return cudaErrorInvalidValue;
   static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
   cudaLaunchConfig_t cfg = {};
