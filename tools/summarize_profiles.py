@@ -79,9 +79,13 @@ def main():
     step = [("fwd", L) for L in layers] + [(p, L) for L in reversed(layers) for p in ("bwd_data", "bwd_filter")]
 
     launches = [l for l in read_launches(os.path.join(a.src, "launches.csv"))
-                if any(t in l["name"] for t in ("nchw_", "generic_", "dbf_kernel", "nhwc_"))]
+                if any(t in l["name"] for t in ("nchw_", "generic_", "dbf_kernel", "nhwc_", "small_", "band_"))]
 
     def kind(name):
+        import re as _re
+        m = _re.search(r"small_fd_kernel<[^>]*,\s*(\d)>", name)
+        if m:  # small-plane kernel: MODE 0 = fwd, 1 = bwd_data
+            return "fwd" if m.group(1) == "0" else "bwd_data"
         if "fwd_kernel" in name or "generic_fwd" in name:
             return "fwd"
         if "bwd_data" in name:
@@ -106,7 +110,8 @@ def main():
         dram = l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0)
         alg = (L.x_elems() + L.y_elems()) * eb + (L.w_elems() * eb if pas != "bwd_filter" else L.w_elems() * 4)
         import re
-        mm = re.search(r"(nchw_\w+_kernel|nhwc_\w+_kernel|dbf_kernel|generic_\w+)<([^>]*)>", l["name"])
+        mm = re.search(r"(nchw_\w+_kernel|nhwc_\w+_kernel|small_\w+_kernel|band_\w+_kernel|dbf_kernel|generic_\w+)<([^>]*)>",
+                       l["name"])
         name = f"{mm.group(1)}<{mm.group(2)}>" if mm else l["name"][:40]
         md.append(f"| {i} | {L.name} | {pas} | {name} | {t_ns / 1e3:.2f} | {100 * t_ns / tot:.1f}% | {dram / 1e6:.1f} | "
                   f"{alg / 1e6:.1f} | {alg / t_ns:.0f} |")
@@ -126,6 +131,8 @@ def main():
         else:
             out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(out.splitlines()))
+        if len(rows) < 3:
+            continue  # capture failed (no matching launch)
         h, u, v = rows[0], rows[1], rows[2]
         d = {h[i]: (v[i], u[i]) for i in range(len(h))}
         md = [f"# ncu --set full: {tag} ({d.get('Kernel Name', ('?',))[0][:120]})", "",
