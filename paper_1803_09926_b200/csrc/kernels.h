@@ -31,6 +31,7 @@ struct SmallPlan {
   int64_t ntasks;
   int groups, nslices, nps, max_chain;
   size_t ws_bytes;
+  int S;  // stride of the small-plane kernels
   // band bwd_filter for large planes (band_bf_kernel)
   bool band;
   int R, V, nbands, cpg;

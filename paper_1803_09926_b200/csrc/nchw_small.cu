@@ -472,6 +472,224 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
   }
 }
 
+// ------------------------------------------------------------ stride 2
+// Input planes W x W (W in {14, 28}), output Wo = W / 2 = 7 V.  Lane (plane l/7,
+// column group) owns V output columns = 2V input columns + the left halo;
+// each output row consumes two new input rows (the window keeps row 2r-1).
+template <class T, int V>
+__device__ __forceinline__ void load_row2(const T* row, int c0, float* xv) {  // x[2c0-1 .. 2c0+2V-1]
+  float v[2 * V];
+  VecIO<T, 2 * V>::load(row + 2 * c0, v);
+#pragma unroll
+  for (int u = 0; u < 2 * V; ++u) xv[1 + u] = v[u];
+  xv[0] = (c0 > 0) ? Elem<T>::load(row + 2 * c0 - 1) : 0.f;
+}
+
+template <class T, int W>
+__global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
+  constexpr int Wo = W / 2, V = Wo / 7, HW = W * W, HWo = Wo * Wo, NXW = 2 * V + 1;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = lane / 7, cg = lane - pl * 7;
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const T* __restrict__ in = static_cast<const T*>(a.in);
+  T* __restrict__ out = static_cast<T*>(a.out);
+  const T* __restrict__ wt = static_cast<const T*>(a.w);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * nwarps;
+  const uint32_t task_bytes = 4u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int64_t t, int s) {
+    if (lane == 0 && t < a.ntasks) {
+      mbar_arrive_expect_tx(&bars[s], task_bytes);
+      bulk_g2s(slot(s), in + t * 4 * HW, task_bytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = gw; t < a.ntasks; t += stride) {
+    const int64_t q = t * 4 + pl;
+    const int c = (int)(q % a.C);
+    float wr[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wr[k] = Elem<T>::ldg(wt + (int64_t)c * 9 + k);
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      const T* pln = slot(s) + pl * HW;
+      float xw[3][NXW];
+#pragma unroll
+      for (int u = 0; u < NXW; ++u) xw[0][u] = 0.f;  // input row -1
+      T* po = out + q * HWo + c0;
+#pragma unroll
+      for (int r = 0; r < Wo; ++r) {
+        load_row2<T, V>(pln + (2 * r) * W, c0, xw[1]);
+        if (2 * r + 1 < W) load_row2<T, V>(pln + (2 * r + 1) * W, c0, xw[2]);
+        else
+#pragma unroll
+          for (int u = 0; u < NXW; ++u) xw[2][u] = 0.f;
+        float o[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          float acc = wr[0] * xw[0][2 * u];
+#pragma unroll
+          for (int k = 1; k < 9; ++k) acc = fmaf(wr[k], xw[k / 3][2 * u + k % 3], acc);
+          o[u] = acc;
+        }
+        VecIO<T, V>::store(po + r * Wo, o);
+#pragma unroll
+        for (int u = 0; u < NXW; ++u) xw[0][u] = xw[2][u];
+      }
+    }
+    __syncwarp();
+    issue(t + a.ns * stride, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  griddep_launch_dependents();
+}
+
+template <class T, int W>
+__global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
+  constexpr int Wo = W / 2, V = Wo / 7, HW = W * W, HWo = Wo * Wo, NXW = 2 * V + 1;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = lane / 7, cg = lane - pl * 7;
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
+  const int cb = g * 4;
+  const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const uint32_t xbytes = 4u * HW * (uint32_t)sizeof(T), dbytes = 4u * HWo * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int n, int s) {
+    if (lane == 0 && n < n1) {
+      mbar_arrive_expect_tx(&bars[s], xbytes + dbytes);
+      bulk_g2s(slot(s), x + ((int64_t)n * a.C + cb) * HW, xbytes, &bars[s]);
+      bulk_g2s(slot(s) + 4 * HW, dy + ((int64_t)n * a.C + cb) * HWo, dbytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
+  float run[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) run[k] = 0.f;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int n = n0 + warp; n < n1; n += nwarps) {
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      const T* pln = slot(s) + pl * HW;
+      const T* pd = slot(s) + 4 * HW + pl * HWo;
+      float xw[3][NXW];
+#pragma unroll
+      for (int u = 0; u < NXW; ++u) xw[0][u] = 0.f;
+      float loc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) loc[k] = 0.f;
+#pragma unroll
+      for (int r = 0; r < Wo; ++r) {
+        load_row2<T, V>(pln + (2 * r) * W, c0, xw[1]);
+        if (2 * r + 1 < W) load_row2<T, V>(pln + (2 * r + 1) * W, c0, xw[2]);
+        else
+#pragma unroll
+          for (int u = 0; u < NXW; ++u) xw[2][u] = 0.f;
+        float d[V];
+        VecIO<T, V>::load(pd + r * Wo + c0, d);
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+#pragma unroll
+          for (int u = 0; u < V; ++u) loc[k] = fmaf(xw[k / 3][2 * u + k % 3], d[u], loc[k]);
+#pragma unroll
+        for (int u = 0; u < NXW; ++u) xw[0][u] = xw[2][u];
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) run[k] += loc[k];
+    }
+    __syncwarp();
+    issue(n + a.ns * nwarps, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  griddep_launch_dependents();
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem + 64 * nwarps);
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) red[(warp * 32 + lane) * 9 + k] = run[k];
+  }
+  __syncthreads();
+  float* part = a.ws_part + (int64_t)sl * a.C * 9;
+  for (int e = threadIdx.x; e < 4 * 9; e += blockDim.x) {
+    const int p = e / 9, k = e - p * 9;
+    float tot = 0.f;
+    for (int wv = 0; wv < nwarps; ++wv) {
+      float v = red[(wv * 32 + p * 7) * 9 + k];
+      for (int l = 1; l < 7; ++l) v += red[(wv * 32 + p * 7 + l) * 9 + k];
+      tot = (wv == 0) ? v : tot + v;
+    }
+    part[(int64_t)(cb + p) * 9 + k] = tot;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
+    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int64_t e0 = (int64_t)cb * 9;
+    const int64_t sstride = (int64_t)a.C * 9;
+    for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) {
+      float stk[16];
+      int top = 0;
+      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
+        float vals[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int s2 = s0 + u;
+          if (s2 < a.nslices) {
+            float cur = vals[u];
+            int bits = s2;
+            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+            stk[top++] = cur;
+          }
+        }
+      }
+      float tot = stk[--top];
+      while (top > 0) tot = stk[--top] + tot;
+      a.dw[e0 + idx] = tot;
+    }
+    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  }
+}
+
 using SKernelFn = void (*)(SArgs);
 
 template <class T, int S, int R>
@@ -505,7 +723,14 @@ SKernelFn pick(int pass, int W) {
     default: return nullptr;
   }
 }
-SKernelFn kernel_for(int dtype, int pass, int W) {
+template <class T>
+SKernelFn pick2(int pass, int W) {  // stride 2: fwd and bwd_filter
+  if (pass == 0) return W == 14 ? small_fwd2_kernel<T, 14> : W == 28 ? small_fwd2_kernel<T, 28> : nullptr;
+  if (pass == 2) return W == 14 ? small_bf2_kernel<T, 14> : W == 28 ? small_bf2_kernel<T, 28> : nullptr;
+  return nullptr;
+}
+SKernelFn kernel_for(int dtype, int pass, int W, int S = 1) {
+  if (S == 2) return dtype == DWCONV_F32 ? pick2<float>(pass, W) : pick2<__nv_bfloat16>(pass, W);
   return dtype == DWCONV_F32 ? pick<float>(pass, W) : pick<__nv_bfloat16>(pass, W);
 }
 
@@ -523,22 +748,28 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   using namespace small;
   static const int on = env_int("DWCONV_SMALL", 1, 0, 1);
   if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
-  if (g.sh != 1 || g.sw != 1 || g.H != g.W || (g.W != 7 && g.W != 14 && g.W != 28)) return false;
+  const int S = g.sh;
+  if (g.sw != S || g.H != g.W) return false;
+  if (S == 1 && g.W != 7 && g.W != 14 && g.W != 28) return false;
+  if (S == 2 && ((g.W != 14 && g.W != 28) || pass == 1 || pass == 3)) return false;  // s2: fwd, bwd_filter
+  if (S != 1 && S != 2) return false;
   if (g.C % 4 != 0 || g.N < 1) return false;
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
   const int64_t task_bytes = 4 * g.H * g.W * eb;
-  if (task_bytes % 16 != 0) return false;  // bulk copies: 16-B granules (bf16 7x7 takes the chunk kernels)
+  const int64_t dy_bytes = 4 * g.Ho * g.Wo * eb;
+  if (task_bytes % 16 != 0 || (pass >= 2 && dy_bytes % 16 != 0)) return false;  // bulk copies: 16-B granules
   *p = SmallPlan{};
   static const int warps_env = env_int("DWCONV_SMALL_WARPS", 4, 1, 8);
   static const int ns_env = env_int("DWCONV_SMALL_STAGES", 3, 2, 6);
   p->warps = warps > 0 ? warps : warps_env;
   p->ns = stages > 0 ? stages : ns_env;
   const bool bf = pass >= 2;  // bwd_filter or the fused backward
-  p->slot_bytes = (uint32_t)((bf ? 2 : 1) * task_bytes);
+  p->slot_bytes = (uint32_t)(task_bytes + (bf ? dy_bytes : 0));
+  p->S = S;
   p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
   if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * 9 * 4);
   if (p->smem > smem_optin - 1024) return false;
-  SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W);
+  SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W, S);
   if (!fn) return false;
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
@@ -568,7 +799,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   const int64_t per_warp = (nps + p->warps - 1) / p->warps;
   int ls = 0;
   while ((1ll << ls) < nsl) ++ls;
-  p->max_chain = (int)(g.W * (g.W / 7) + per_warp + 7 + p->warps + 2 * ls + 1);
+  p->max_chain = (int)(g.Wo * (g.Wo / 7) + per_warp + 7 + p->warps + 2 * ls + 1);
   const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
   p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
   return p->max_chain <= 160;
@@ -642,7 +873,7 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   }
-  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R) : kernel_for(g.dtype, pass, (int)g.W);
+  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R) : kernel_for(g.dtype, pass, (int)g.W, p.S);
   if (!fn) return cudaErrorInvalidValue;
   static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
   cudaLaunchConfig_t cfg = {};
