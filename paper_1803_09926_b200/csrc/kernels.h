@@ -32,6 +32,7 @@ struct SmallPlan {
   int groups, nslices, nps, max_chain;
   size_t ws_bytes;
   int S;  // stride of the small-plane kernels
+  int occ, sms;  // resident CTAs per SM, SMs (early PDL only when the grid is one wave)
   // band bwd_filter for large planes (band_bf_kernel)
   bool band;
   int R, V, nbands, cpg;

@@ -44,6 +44,7 @@ struct SArgs {
   int groups, nslices, nps;  // bwd_filter
   // band bwd_filter (band_bf_kernel)
   int H, W, Ho, Wo, nbands, cpg;  // cpg: channels per group (one per warp)
+  int early_pdl;                   // trigger the dependent launch once the ring is primed
 };
 
 // one row of the window: the lane's V columns and the two halo columns
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
   int s = 0;
   uint32_t ph = 0;
   for (int64_t t = gw; t < a.ntasks; t += stride) {
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
     issue(t + a.ns * stride, s);  // the slot is free: every lane is past it
     if (++s == a.ns) { s = 0; ph ^= 1; }
   }
-  griddep_launch_dependents();
+  if (!a.early_pdl) griddep_launch_dependents();
 }
 
 // FUSED: also dx = the forward stencil over the staged dy with the rotated kernel
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
+  if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
   float wf[FUSED ? 9 : 1];  // rotated kernel of this lane's channel (fused dx)
   if constexpr (FUSED) {
     const T* __restrict__ wt = static_cast<const T*>(a.w);
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
     issue(n + a.ns * nwarps, s);
     if (++s == a.ns) { s = 0; ph ^= 1; }
   }
-  griddep_launch_dependents();
+  if (!a.early_pdl) griddep_launch_dependents();
   // ---- lanes of a plane in order, then warps in order -> the slice partial
   __syncthreads();
   float* red = reinterpret_cast<float*>(smem + 64 * nwarps);  // [warp][lane][9]; the ring is idle now
@@ -357,6 +360,7 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(i, i);
+  if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
   const int c0 = lane * V;
   float run[9];
 #pragma unroll
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
     issue(t + a.ns, s);
     if (++s == a.ns) { s = 0; ph ^= 1; }
   }
-  griddep_launch_dependents();
+  if (!a.early_pdl) griddep_launch_dependents();
   // ---- lanes: fixed xor tree (lanes >= 28 hold zeros) -> the warp's channel partial
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
@@ -516,6 +520,7 @@ __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
   int s = 0;
   uint32_t ph = 0;
   for (int64_t t = gw; t < a.ntasks; t += stride) {
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
     issue(t + a.ns * stride, s);
     if (++s == a.ns) { s = 0; ph ^= 1; }
   }
-  griddep_launch_dependents();
+  if (!a.early_pdl) griddep_launch_dependents();
 }
 
 template <class T, int W>
@@ -591,6 +596,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
+  if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
   float run[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) run[k] = 0.f;
@@ -630,7 +636,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
     issue(n + a.ns * nwarps, s);
     if (++s == a.ns) { s = 0; ph ^= 1; }
   }
-  griddep_launch_dependents();
+  if (!a.early_pdl) griddep_launch_dependents();
   __syncthreads();
   float* red = reinterpret_cast<float*>(smem + 64 * nwarps);
   if (live) {
@@ -779,6 +785,8 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * p->warps, p->smem) != cudaSuccess || occ < 1)
     return false;
+  p->occ = occ;
+  p->sms = num_sms;
   if (!bf) {
     p->ntasks = g.N * g.C / 4;
     p->grid = (int)std::min<int64_t>((p->ntasks + p->warps - 1) / p->warps, (int64_t)occ * num_sms);
@@ -836,6 +844,8 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * warps, p->smem) != cudaSuccess || occ < 1)
     return false;
+  p->occ = occ;
+  p->sms = num_sms;
   p->nbands = (int)((g.Ho + rows - 1) / rows);
   p->cpg = warps;
   p->groups = (int)((g.C + warps - 1) / warps);
@@ -863,6 +873,8 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
   SArgs a{};
   a.H = (int)g.H; a.W = (int)g.W; a.Ho = (int)g.Ho; a.Wo = (int)g.Wo;
   a.nbands = p.nbands; a.cpg = p.cpg;
+  static const int early = env_int("DWCONV_SMALL_EARLY_PDL", 0, 0, 1);
+  a.early_pdl = early && (int64_t)p.grid <= (int64_t)p.occ * p.sms;
   a.in = in; a.in2 = in2; a.out = out; a.w = w; a.dw = dw;
   a.ntasks = p.ntasks;
   a.C = (int)g.C; a.N = (int)g.N;
