@@ -470,6 +470,70 @@ __device__ __forceinline__ void stencil_strip_pair(const __nv_bfloat16* spa, con
   }
 }
 
+
+// Two-level deterministic cross-CTA reduction of per-slice partials (no float
+// atomics).  Every CTA of channel block `gid` has written its slice partial
+// part[sl * sstride + e0 + i] (i < nvals), issued __threadfence() and
+// __syncthreads(); then all its threads call this.  Level 1: the last CTA (integer
+// ticket) of each group of 32 consecutive slices sums the group's partials
+// pairwise in slice order into l2[sg]; level 2: the last group finisher sums
+// l2[0..ngrp) pairwise in group order into dw.  Each level is <= 32 dependent
+// loads deep instead of one flat pass over hundreds of slices.  Both levels hand
+// back zeroed partials and tickets.
+__device__ __forceinline__ float pairwise_sum_strided(float* base, int64_t stride, int count) {
+  float stk[8];
+  int top = 0;
+  for (int s0 = 0; s0 < count; s0 += 16) {
+    float vals[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) vals[u] = (s0 + u < count) ? __ldcg(base + (s0 + u) * stride) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (s0 + u < count) __stcg(base + (s0 + u) * stride, 0.f);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int s2 = s0 + u;
+      if (s2 < count) {
+        float cur = vals[u];
+        int bits = s2;
+        while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
+        stk[top++] = cur;
+      }
+    }
+  }
+  float tot = stk[--top];
+  while (top > 0) tot = stk[--top] + tot;
+  return tot;
+}
+
+__device__ __forceinline__ void finalize_two_level(float* part, float* l2, unsigned* t1, unsigned* t2, int gid,
+                                                   int sl, int nslices, int64_t sstride, int64_t e0, int nvals,
+                                                   float* dw, unsigned* s_flag) {
+  const int ngrp = (nslices + 31) / 32;
+  const int sg = sl / 32;
+  const int gsz = min(32, nslices - sg * 32);
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&t1[(int64_t)gid * ngrp + sg], 1u);
+    *s_flag = (prev == (unsigned)(gsz - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!*s_flag) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < nvals; i += blockDim.x)
+    __stcg(l2 + sg * sstride + e0 + i, pairwise_sum_strided(part + (int64_t)sg * 32 * sstride + e0 + i, sstride, gsz));
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t1[(int64_t)gid * ngrp + sg] = 0u;
+    const unsigned prev = atomicAdd(&t2[gid], 1u);
+    *s_flag = (prev == (unsigned)(ngrp - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!*s_flag) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < nvals; i += blockDim.x) dw[e0 + i] = pairwise_sum_strided(l2 + e0 + i, sstride, ngrp);
+  if (threadIdx.x == 0) t2[gid] = 0u;
+}
 }  // namespace nchw
 
 namespace direct {

@@ -419,44 +419,9 @@ __global__ void __launch_bounds__(kMaxConsumers + 32) nhwc_tma_bf_kernel(const _
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
-    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int64_t e0 = (int64_t)g * a.CB * 9;
-    const int nvals = a.CB * 9;
-    const int64_t sstride = (int64_t)C * 9;
-    for (int idx = threadIdx.x; idx < nvals; idx += blockDim.x) {
-      float stk[16];
-      int top = 0;
-      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
-        float vals[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int s2 = s0 + u;
-          if (s2 < a.nslices) {
-            float cur = vals[u];
-            int bits = s2;
-            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
-            stk[top++] = cur;
-          }
-        }
-      }
-      float tot = stk[--top];
-      while (top > 0) tot = stk[--top] + tot;
-      a.dw[e0 + idx] = tot;
-    }
-    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
-  }
+  const int ngrp = (a.nslices + 31) / 32;
+  nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * C * 9, a.ws_ticket, a.ws_ticket + a.ncb * ngrp,
+                           g, sl, a.nslices, (int64_t)C * 9, (int64_t)g * a.CB * 9, a.CB * 9, a.dw, &s_last);
 }
 
 using BKernelFn = void (*)(const CUtensorMap, const CUtensorMap, const BArgs);
@@ -737,8 +702,11 @@ bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p
   int ls = 0;
   while ((1ll << ls) < nsl) ++ls;
   p->max_chain = TH + (int)tps + lt + 2 * ls + 1;
-  const size_t tick = ((size_t)p->ncb * 4 + 15) / 16 * 16;
-  p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
+  // workspace: level-1 tickets [ncb][groups of 32 slices] + level-2 tickets [ncb],
+  // slice partials [nslices][C][9], group partials [groups][C][9]
+  const int64_t ngrp = (nsl + 31) / 32;
+  const size_t tick = ((size_t)(p->ncb * ngrp + p->ncb) * 4 + 15) / 16 * 16;
+  p->ws_bytes = tick + (size_t)(nsl + ngrp) * g.C * 9 * 4;
   return p->max_chain <= 160;
 }
 
@@ -772,7 +740,8 @@ cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* 
   }
   BArgs a{};
   a.dw = dw;
-  const size_t tick = ((size_t)p.ncb * 4 + 15) / 16 * 16;
+  const int64_t ngrp = (p.nslices + 31) / 32;
+  const size_t tick = ((size_t)(p.ncb * ngrp + p.ncb) * 4 + 15) / 16 * 16;
   a.ws_ticket = static_cast<unsigned*>(ws);
   a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   a.N = (int)g.N; a.C = (int)g.C; a.CB = p.CB; a.NCV = p.NCV; a.TW = p.TW;
