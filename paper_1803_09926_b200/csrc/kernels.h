@@ -24,6 +24,17 @@ cudaError_t launch_generic_fwd(const Geom& g, const void* x, const void* w, void
 cudaError_t launch_generic_bwd_data(const Geom& g, const void* dy, const void* w, void* dx, cudaStream_t st);
 cudaError_t launch_generic_bwd_filter(const Geom& g, const void* x, const void* dy, float* dw, cudaStream_t st);
 
+// Workspace of the two-level slice finalize (nchw_common.cuh finalize_two_level):
+// level-1 tickets [groups][ceil(slices/32)] + level-2 tickets [groups] (16-B
+// rounded), then slice partials [slices][C][9] and group partials [ceil(slices/32)][C][9].
+inline size_t two_level_tick_bytes(int64_t groups, int64_t slices) {
+  const int64_t ngrp = (slices + 31) / 32;
+  return ((size_t)(groups * ngrp + groups) * 4 + 15) / 16 * 16;
+}
+inline size_t two_level_ws_bytes(int64_t groups, int64_t slices, int64_t channels, int64_t taps = 9) {
+  return two_level_tick_bytes(groups, slices) + (size_t)(slices + (slices + 31) / 32) * channels * taps * 4;
+}
+
 // ---- NCHW small-plane warp-task kernels (W = H in {7,14,28}, 3x3 s1 p1 m1): nchw_small.cu
 struct SmallPlan {
   int warps, ns, grid, smem;

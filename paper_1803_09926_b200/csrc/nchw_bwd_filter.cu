@@ -262,44 +262,11 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
-    *s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (*s_last) {
-    __threadfence();
-    const int nvals = np * m * KK;
-    float* base = a.ws_part + (int64_t)c0ch * m * KK;
-    const int64_t sstride = (int64_t)Co * KK;
-    for (int idx = threadIdx.x; idx < nvals; idx += (int)blockDim.x) {
-      // pairwise (binary-counter) summation over slices in slice order; loads
-      // are issued 8 at a time so their latencies overlap.
-      float stk[8];
-      int top = 0;
-      for (int s0 = 0; s0 < a.nslices; s0 += 8) {
-        float vals[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) vals[u] = (s0 + u < a.nslices) ? __ldcg(base + (s0 + u) * sstride + idx) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (s0 + u < a.nslices) __stcg(base + (s0 + u) * sstride + idx, 0.f);  // hand back zero-filled
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int s = s0 + u;
-          if (s < a.nslices) {
-            float cur = vals[u];
-            int bits = s;
-            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
-            stk[top++] = cur;
-          }
-        }
-      }
-      float tot = stk[--top];
-      while (top > 0) tot = stk[--top] + tot;
-      a.dw[(int64_t)c0ch * m * KK + idx] = tot;
-    }
-    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;  // leave the workspace zeroed
+  {  // two-level slice finalize (nchw_common.cuh): groups of 32 slices, then groups
+    const int ngrp = (a.nslices + 31) / 32;
+    finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * Co * KK, a.ws_ticket,
+                       a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)Co * KK,
+                       (int64_t)c0ch * m * KK, np * m * KK, a.dw, s_last);
   }
 }
 

@@ -519,6 +519,11 @@ __device__ __forceinline__ void finalize_two_level(float* part, float* l2, unsig
   __syncthreads();
   if (!*s_flag) return;
   __threadfence();
+  if (ngrp == 1) {  // <= 32 slices: one level, straight into dw
+    for (int i = threadIdx.x; i < nvals; i += blockDim.x) dw[e0 + i] = pairwise_sum_strided(part + e0 + i, sstride, gsz);
+    if (threadIdx.x == 0) t1[gid] = 0u;
+    return;
+  }
   for (int i = threadIdx.x; i < nvals; i += blockDim.x)
     __stcg(l2 + sg * sstride + e0 + i, pairwise_sum_strided(part + (int64_t)sg * 32 * sstride + e0 + i, sstride, gsz));
   __threadfence();

@@ -224,8 +224,7 @@ static bool plan_direct_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p, int
   const int64_t per_task = (int64_t)R * (packed ? V / 2 : V) + (packed ? 1 : 0);
   const int64_t task_sum = (nps * nsb + spc - 1) / spc;
   p->max_chain = (int)(per_task + task_sum + L + spc + 2 * nchw::ilog2_ceil(nsl) + 1);
-  const size_t tick = ((size_t)groups * 4 + 15) / 16 * 16;
-  p->ws_bytes = tick + (size_t)nsl * Co * 9 * 4;
+  p->ws_bytes = two_level_ws_bytes(groups, nsl, Co);
   return p->max_chain <= 160 && groups * nsl < (int64_t)1 << 31;
 }
 
@@ -518,8 +517,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     const int64_t per_chunk = strips_per_thread * R * (packed ? c->V / 2 : c->V) + (packed ? 1 : 0);
     const int64_t thread_sum = (c->tpg <= 32) ? c->tpg : (c->tpg + 31) / 32 + 5;
     c->max_chain = (int)(per_chunk + nps * nb + thread_sum + 2 * ilog2_ceil(nsl) + 1);
-    const size_t tick = ((size_t)c->groups * 4 + 15) / 16 * 16;
-    c->ws_bytes = tick + (size_t)nsl * g.C * m * KK * 4;
+    c->ws_bytes = two_level_ws_bytes(c->groups, nsl, g.C * m, KK);
     return nsl <= 128 && c->max_chain <= 160;
   };
   *p = bestp;
@@ -660,7 +658,7 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
 cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void* x, const void* dy, float* dw,
                                    void* ws, cudaStream_t st) {
   if (p.small) return launch_nchw_small(g, p.sp, 2, x, dy, nullptr, nullptr, dw, ws, st);
-  const size_t tk = ((size_t)p.groups * 4 + 15) / 16 * 16;
+  const size_t tk = two_level_tick_bytes(p.groups, p.nslices);
   if (p.direct) {
     direct::DArgs d{};
     d.x = x; d.dy = dy; d.dw = dw;
@@ -690,7 +688,7 @@ cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void
   }
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.in2 = dy; a.dw = dw;
-  const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
+  const size_t tick = two_level_tick_bytes(p.groups, p.nslices);
   a.ws_ticket = static_cast<unsigned*>(ws);
   a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   nchw::KernelFn fn = nchw::bwd_filter_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);
@@ -702,7 +700,7 @@ cudaError_t launch_nchw_bwd_fused(const Geom& g, const ChunkPlan& p, const void*
   if (p.small) return launch_nchw_small(g, p.sp, 3, x, dy, w, dx, dw, ws, st);
   nchw::NArgs a = base_args(g, p);
   a.in = x; a.in2 = dy; a.dw = dw; a.w = w; a.out = dx;
-  const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
+  const size_t tick = two_level_tick_bytes(p.groups, p.nslices);
   a.ws_ticket = static_cast<unsigned*>(ws);
   a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   nchw::KernelFn fn = nchw::bwd_fused_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded);

@@ -265,42 +265,11 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
-    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int64_t e0 = (int64_t)cb * 9;
-    const int64_t sstride = (int64_t)a.C * 9;
-    for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) {
-      float stk[16];
-      int top = 0;
-      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
-        float vals[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int s2 = s0 + u;
-          if (s2 < a.nslices) {
-            float cur = vals[u];
-            int bits = s2;
-            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
-            stk[top++] = cur;
-          }
-        }
-      }
-      float tot = stk[--top];
-      while (top > 0) tot = stk[--top] + tot;
-      a.dw[e0 + idx] = tot;
-    }
-    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  {
+    const int ngrp = (a.nslices + 31) / 32;
+    nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
+                             a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
+                             (int64_t)cb * 9, 36, a.dw, &s_last);
   }
 }
 
@@ -436,43 +405,11 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
-    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int64_t e0 = (int64_t)g * a.cpg * 9;
-    const int nvals = min(a.cpg, a.C - g * a.cpg) * 9;
-    const int64_t sstride = (int64_t)a.C * 9;
-    for (int idx = threadIdx.x; idx < nvals; idx += blockDim.x) {
-      float stk[16];
-      int top = 0;
-      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
-        float vals[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int s2 = s0 + u;
-          if (s2 < a.nslices) {
-            float cur = vals[u];
-            int bits = s2;
-            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
-            stk[top++] = cur;
-          }
-        }
-      }
-      float tot = stk[--top];
-      while (top > 0) tot = stk[--top] + tot;
-      a.dw[e0 + idx] = tot;
-    }
-    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  {
+    const int ngrp = (a.nslices + 31) / 32;
+    nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
+                             a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
+                             (int64_t)g * a.cpg * 9, min(a.cpg, a.C - g * a.cpg) * 9, a.dw, &s_last);
   }
 }
 
@@ -657,42 +594,11 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&a.ws_ticket[g], 1u);
-    s_last = (prev == (unsigned)(a.nslices - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int64_t e0 = (int64_t)cb * 9;
-    const int64_t sstride = (int64_t)a.C * 9;
-    for (int idx = threadIdx.x; idx < 36; idx += blockDim.x) {
-      float stk[16];
-      int top = 0;
-      for (int s0 = 0; s0 < a.nslices; s0 += 16) {
-        float vals[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          vals[u] = (s0 + u < a.nslices) ? __ldcg(a.ws_part + (s0 + u) * sstride + e0 + idx) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (s0 + u < a.nslices) __stcg(a.ws_part + (s0 + u) * sstride + e0 + idx, 0.f);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int s2 = s0 + u;
-          if (s2 < a.nslices) {
-            float cur = vals[u];
-            int bits = s2;
-            while (bits & 1) { cur = stk[--top] + cur; bits >>= 1; }
-            stk[top++] = cur;
-          }
-        }
-      }
-      float tot = stk[--top];
-      while (top > 0) tot = stk[--top] + tot;
-      a.dw[e0 + idx] = tot;
-    }
-    if (threadIdx.x == 0) a.ws_ticket[g] = 0u;
+  {
+    const int ngrp = (a.nslices + 31) / 32;
+    nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
+                             a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
+                             (int64_t)cb * 9, 36, a.dw, &s_last);
   }
 }
 
@@ -808,8 +714,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   int ls = 0;
   while ((1ll << ls) < nsl) ++ls;
   p->max_chain = (int)(g.Wo * (g.Wo / 7) + per_warp + 7 + p->warps + 2 * ls + 1);
-  const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
-  p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
+  p->ws_bytes = two_level_ws_bytes(p->groups, nsl, g.C);
   return p->max_chain <= 160;
 }
 
@@ -862,8 +767,7 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   int ls = 0;
   while ((1ll << ls) < nsl) ++ls;
   p->max_chain = (int)(rows * V + nps * p->nbands + 5 + 2 * ls + 1);
-  const size_t tick = ((size_t)p->groups * 4 + 15) / 16 * 16;
-  p->ws_bytes = tick + (size_t)nsl * g.C * 9 * 4;
+  p->ws_bytes = two_level_ws_bytes(p->groups, nsl, g.C);
   return p->max_chain <= 160;
 }
 
@@ -881,7 +785,7 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
   a.ns = p.ns; a.slot_bytes = p.slot_bytes;
   a.groups = p.groups; a.nslices = p.nslices; a.nps = p.nps;
   if (pass >= 2) {
-    const size_t tick = ((size_t)p.groups * 4 + 15) / 16 * 16;
+    const size_t tick = two_level_tick_bytes(p.groups, p.nslices);
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   }
