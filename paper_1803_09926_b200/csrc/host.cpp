@@ -403,10 +403,12 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     if (dp.variant == DWCONV_VARIANT_NCHW_CHUNK) cands.push_back(dp.chunk);
     if (pass == DWCONV_PASS_BWD_FILTER && g.dtype <= DWCONV_BF16) {
       // band bwd_filter for large planes: {warps, ring slots, band rows}
-      static const int bshapes[][3] = {{4, 2, 7}, {4, 3, 7}, {8, 2, 7}, {2, 3, 7}, {4, 2, 14}, {8, 2, 14}};
+      // {warps, ring slots, band rows, planes per warp}
+      static const int bshapes[][4] = {{4, 2, 7, 1}, {4, 3, 7, 1}, {8, 2, 7, 1}, {2, 3, 7, 1}, {4, 2, 14, 1},
+                                       {8, 2, 14, 1}, {4, 2, 7, 2}, {4, 3, 7, 2}, {8, 2, 7, 2}, {4, 2, 14, 2}};
       for (const auto& sh : bshapes) {
         ChunkPlan v;
-        if (dwk::band_chunk_plan(g, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2])) cands.push_back(v);
+        if (dwk::band_chunk_plan(g, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2], sh[3])) cands.push_back(v);
       }
     }
     std::vector<ChunkPlan> more;
@@ -435,7 +437,8 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         for (const ChunkPlan& o : cands)
           dup = dup || (o.P == c.P && o.nbands == c.nbands && o.band_rows == c.band_rows && o.threads == c.threads &&
                         o.tpg == c.tpg && o.ns == c.ns && o.pair == c.pair && o.direct == c.direct &&
-                        o.small == c.small && o.sp.band == c.sp.band && o.nslices == c.nslices && o.grid == c.grid);
+                        o.small == c.small && o.sp.band == c.sp.band && o.sp.ppw == c.sp.ppw && o.nslices == c.nslices &&
+                        o.grid == c.grid);
         if (!dup) cands.push_back(c);
       }
     }

@@ -46,9 +46,10 @@ struct SmallPlan {
   int occ, sms;  // resident CTAs per SM, SMs (early PDL only when the grid is one wave)
   // band bwd_filter for large planes (band_bf_kernel)
   bool band;
-  int R, V, nbands, cpg;
+  int R, V, nbands, cpg, ppw;
 };
-bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* plan, int warps, int stages, int rows);
+bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* plan, int warps, int stages, int rows,
+                       int ppw = 1);
 // warps / stages: CTA size and per-warp ring depth (0 = the defaults, env DWCONV_SMALL_WARPS / _STAGES)
 // slices (bwd_filter): batch slices per channel group (0 = about one wave of CTAs)
 bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* plan, int warps = 0,
@@ -104,7 +105,8 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
                std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
 bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps = 0,
                       int stages = 0, int slices = 0);
-bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* plan, int warps, int stages, int rows);
+bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* plan, int warps, int stages, int rows,
+                     int ppw = 1);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,
                             cudaStream_t st);
 cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* dy, const void* w, void* dx,

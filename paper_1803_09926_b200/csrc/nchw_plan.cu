@@ -613,16 +613,17 @@ bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, Chun
   return true;
 }
 
-bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages, int rows) {
+bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages, int rows,
+                     int ppw) {
   SmallPlan sp;
-  if (!plan_nchw_band_bf(g, num_sms, smem_optin, &sp, warps, stages, rows)) return false;
+  if (!plan_nchw_band_bf(g, num_sms, smem_optin, &sp, warps, stages, rows, ppw)) return false;
   *p = ChunkPlan{};
   p->small = true;
   p->sp = sp;
   p->threads = 32 * sp.warps;
   p->grid = sp.grid;
   p->smem_bytes = sp.smem;
-  p->P = 1;
+  p->P = sp.ppw;
   p->nbands = sp.nbands;
   p->band_rows = sp.R;
   p->ns = sp.ns;

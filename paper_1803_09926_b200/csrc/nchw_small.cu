@@ -284,9 +284,12 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
 // Deterministic reduction: R*V terms per task -> running sum over the warp's
 // tasks -> xor-shuffle tree over the 32 lanes -> per-slice partial -> ticketed
 // pairwise finalize over slices (as above).
-template <class T, int S, int V, int R>
+template <class T, int S, int V, int R, int PPW = 1>
 __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
+  // PPW planes (consecutive channels) per warp: lanes [16p, 16p + Wo/V) own plane p
+  // when PPW = 2 (Wo = 14 V), lanes [0, 28) when PPW = 1 (Wo = 28 V)
   constexpr int NX = S * V;  // own x columns per lane (stride 2: + the left halo only)
+  constexpr int LPP = 32 / PPW;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -294,15 +297,19 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
   const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
-  const int c = g * a.cpg + warp;  // this warp's channel
-  const bool wlive = warp < a.cpg && c < a.C;
-  const bool live = wlive && lane < 28;
+  const int cw = g * a.cpg + warp * PPW;  // first channel of this warp
+  const int pl = lane / LPP, li = lane - pl * LPP;
+  const int c = cw + pl;                  // this lane's channel
+  const int np_w = max(0, min(PPW, min(a.cpg - warp * PPW, a.C - cw)));  // live planes of the warp
+  const bool wlive = np_w > 0;
   const int H = a.H, W = a.W, Ho = a.Ho, Wo = a.Wo;
+  const bool live = pl < np_w && li * V < Wo;
   const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
   const int ntask = (n1 - n0) * a.nbands;
   const T* __restrict__ x = static_cast<const T*>(a.in);
   const T* __restrict__ dy = static_cast<const T*>(a.in2);
-  const uint32_t xcap = (uint32_t)(((R - 1) * S + 3) * W * sizeof(T) + 15) & ~15u;  // x part of a slot
+  const uint32_t xcap = (uint32_t)(((R - 1) * S + 3) * W * sizeof(T) + 15) & ~15u;  // x part of a plane's slot
+  const uint32_t dcap = (uint32_t)(R * Wo * sizeof(T) + 15) & ~15u;
   if (lane == 0) {
     for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
@@ -323,14 +330,17 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
       int n, r0, r1, lo, hi;
       rows_of(t, &n, &r0, &r1, &lo, &hi);
       const uint32_t xb = (uint32_t)((hi - lo) * W * sizeof(T)), db = (uint32_t)((r1 - r0) * Wo * sizeof(T));
-      mbar_arrive_expect_tx(&bars[s], xb + db);
-      bulk_g2s(slot(s), x + (((int64_t)n * a.C + c) * H + lo) * W, xb, &bars[s]);
-      bulk_g2s(slot(s) + xcap, dy + (((int64_t)n * a.C + c) * Ho + r0) * Wo, db, &bars[s]);
+      mbar_arrive_expect_tx(&bars[s], (uint32_t)np_w * (xb + db));
+      for (int p = 0; p < np_w; ++p) {
+        unsigned char* sp = slot(s) + (size_t)p * (xcap + dcap);
+        bulk_g2s(sp, x + (((int64_t)n * a.C + cw + p) * H + lo) * W, xb, &bars[s]);
+        bulk_g2s(sp + xcap, dy + (((int64_t)n * a.C + cw + p) * Ho + r0) * Wo, db, &bars[s]);
+      }
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(i, i);
   if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
-  const int c0 = lane * V;
+  const int c0 = li * V;
   float run[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) run[k] = 0.f;
@@ -341,8 +351,9 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
     if (live) {
       int n, r0, r1, lo, hi;
       rows_of(t, &n, &r0, &r1, &lo, &hi);
-      const T* xs = reinterpret_cast<const T*>(slot(s)) - (int64_t)lo * W;  // x row ih at xs + ih*W (ih in [lo,hi))
-      const T* ds = reinterpret_cast<const T*>(slot(s) + xcap) - (int64_t)r0 * Wo;
+      const unsigned char* sp = slot(s) + (size_t)pl * (xcap + dcap);
+      const T* xs = reinterpret_cast<const T*>(sp) - (int64_t)lo * W;  // x row ih at xs + ih*W (ih in [lo,hi))
+      const T* ds = reinterpret_cast<const T*>(sp + xcap) - (int64_t)r0 * Wo;
       // window rows: x row ih = r*S - 1 + i, i = 0..2; columns S*c0 - 1 .. S*c0 + NX (+1 at S = 1)
       float xw[3][NX + 2];
       auto ldx = [&](int ih, float* v) {
@@ -394,14 +405,14 @@ __global__ void __launch_bounds__(256) band_bf_kernel(const SArgs a) {
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) run[k] += __shfl_xor_sync(0xffffffffu, run[k], off);
+    for (int off = LPP / 2; off > 0; off >>= 1) run[k] += __shfl_xor_sync(0xffffffffu, run[k], off);
   }
   float* part = a.ws_part + (int64_t)sl * a.C * 9;
-  if (wlive && lane < 9) {
+  if (pl < np_w && li < 9) {
     float v = run[0];
 #pragma unroll
-    for (int k = 1; k < 9; ++k) v = (lane == k) ? run[k] : v;
-    part[(int64_t)c * 9 + lane] = v;
+    for (int k = 1; k < 9; ++k) v = (li == k) ? run[k] : v;
+    part[(int64_t)c * 9 + li] = v;
   }
   __threadfence();
   __syncthreads();
@@ -604,23 +615,24 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
 
 using SKernelFn = void (*)(SArgs);
 
-template <class T, int S, int R>
+template <class T, int S, int R, int PPW>
 SKernelFn band_pick_v(int V) {
   switch (V) {
-    case 1: return band_bf_kernel<T, S, 1, R>;
-    case 2: return band_bf_kernel<T, S, 2, R>;
-    case 4: return (S == 1 || sizeof(T) == 2) ? band_bf_kernel<T, S, 4, R> : nullptr;
+    case 1: return PPW == 1 ? band_bf_kernel<T, S, 1, R, PPW> : nullptr;
+    case 2: return band_bf_kernel<T, S, 2, R, PPW>;
+    case 4: return (S == 1 || sizeof(T) == 2) ? band_bf_kernel<T, S, 4, R, PPW> : nullptr;
     default: return nullptr;
   }
 }
-SKernelFn band_kernel_for(int dtype, int S, int V, int R) {
-  if (dtype == DWCONV_F32) {
-    if (S == 1) return R == 7 ? band_pick_v<float, 1, 7>(V) : band_pick_v<float, 1, 14>(V);
-    return R == 7 ? band_pick_v<float, 2, 7>(V) : band_pick_v<float, 2, 14>(V);
-  }
+template <class T, int PPW>
+SKernelFn band_pick_sr(int S, int V, int R) {
+  if (S == 1) return R == 7 ? band_pick_v<T, 1, 7, PPW>(V) : band_pick_v<T, 1, 14, PPW>(V);
+  return R == 7 ? band_pick_v<T, 2, 7, PPW>(V) : band_pick_v<T, 2, 14, PPW>(V);
+}
+SKernelFn band_kernel_for(int dtype, int S, int V, int R, int PPW = 1) {
+  if (dtype == DWCONV_F32) return PPW == 2 ? band_pick_sr<float, 2>(S, V, R) : band_pick_sr<float, 1>(S, V, R);
   using B = __nv_bfloat16;
-  if (S == 1) return R == 7 ? band_pick_v<B, 1, 7>(V) : band_pick_v<B, 1, 14>(V);
-  return R == 7 ? band_pick_v<B, 2, 7>(V) : band_pick_v<B, 2, 14>(V);
+  return PPW == 2 ? band_pick_sr<B, 2>(S, V, R) : band_pick_sr<B, 1>(S, V, R);
 }
 
 template <class T>
@@ -719,26 +731,30 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
 }
 
 // Band bwd_filter for large planes (band_bf_kernel): Wo = 28 V, V in {1, 2, 4}.
-bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages, int rows) {
+bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages, int rows,
+                       int ppw) {
   using namespace small;
   static const int on = env_int("DWCONV_BAND_BF", 1, 0, 1);
   if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
   const int S = g.sh;
-  if (g.sw != S || (S != 1 && S != 2) || g.Wo % 28 != 0 || g.W != S * g.Wo || g.N < 1) return false;
-  const int V = (int)(g.Wo / 28);
+  if (ppw != 1 && ppw != 2) return false;
+  const int lanes = 28 / ppw;  // output columns are split over 28 (one plane) or 14 (two planes) lanes
+  if (g.sw != S || (S != 1 && S != 2) || g.Wo % lanes != 0 || g.W != S * g.Wo || g.N < 1) return false;
+  const int V = (int)(g.Wo / lanes);
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
   if ((g.W * eb) % 16 != 0 || (g.Wo * eb) % 16 != 0 || g.N * g.C >= ((int64_t)1 << 31)) return false;
   if (rows != 7 && rows != 14) return false;
-  SKernelFn fn = band_kernel_for(g.dtype, S, V, rows);
+  SKernelFn fn = band_kernel_for(g.dtype, S, V, rows, ppw);
   if (!fn) return false;
   *p = SmallPlan{};
   p->band = true;
   p->R = rows;
   p->V = V;
+  p->ppw = ppw;
   p->warps = warps;
   p->ns = stages;
   const int64_t xcap = ((((int64_t)rows - 1) * S + 3) * g.W * eb + 15) & ~(int64_t)15;
-  p->slot_bytes = (uint32_t)(xcap + (((int64_t)rows * g.Wo * eb + 15) & ~(int64_t)15));
+  p->slot_bytes = (uint32_t)(ppw * (xcap + (((int64_t)rows * g.Wo * eb + 15) & ~(int64_t)15)));
   p->smem = 64 * warps + warps * stages * (int)p->slot_bytes;
   if (p->smem > smem_optin - 1024) return false;
   cudaFuncAttributes fa{};
@@ -752,8 +768,8 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   p->occ = occ;
   p->sms = num_sms;
   p->nbands = (int)((g.Ho + rows - 1) / rows);
-  p->cpg = warps;
-  p->groups = (int)((g.C + warps - 1) / warps);
+  p->cpg = warps * ppw;
+  p->groups = (int)((g.C + p->cpg - 1) / p->cpg);
   // slices: about one wave, <= 64 tasks (image x band) per warp, <= 128 slices
   int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
   nsl = std::max<int64_t>(nsl, (g.N * p->nbands + 63) / 64);
@@ -766,7 +782,7 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   p->grid = (int)(p->groups * nsl);
   int ls = 0;
   while ((1ll << ls) < nsl) ++ls;
-  p->max_chain = (int)(rows * V + nps * p->nbands + 5 + 2 * ls + 1);
+  p->max_chain = (int)(rows * V + nps * p->nbands + 5 + 2 * ls + 1);  // xor tree: <= 5 levels
   p->ws_bytes = two_level_ws_bytes(p->groups, nsl, g.C);
   return p->max_chain <= 160;
 }
@@ -789,7 +805,7 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   }
-  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R) : kernel_for(g.dtype, pass, (int)g.W, p.S);
+  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R, p.ppw) : kernel_for(g.dtype, pass, (int)g.W, p.S);
   if (!fn) return cudaErrorInvalidValue;
   static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
   cudaLaunchConfig_t cfg = {};
