@@ -172,7 +172,7 @@ typedef struct {
 } dwconv_plan_info;
 DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info);
 
-/* Measurement-driven plan selection (cf. a "find" step): the NCHW chunk family's
+/* Measurement-driven plan selection (cf. a "find" step): the fast kernel families'
  * distinct launch shapes for (d, pass), the planner's default first, then by the
  * planner's score.  The caller times them on its own buffers and installs the
  * fastest with dwconv_plan_select; later calls with the same descriptor and pass
@@ -181,11 +181,11 @@ DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* inf
  * the parity rules of DESIGN.md §5, and a bwd_filter candidate may need a
  * different workspace size (dwconv_bwd_filter_workspace_bytes reflects the
  * selection; re-query after selecting, and zero-fill a new workspace).
- *   dwconv_plan_candidates: pass in {FWD, BWD_DATA, BWD_FILTER, BWD (fused backward;
- *     dwconv_bwd_workspace_bytes reflects its selection)}; writes at most
+ *   dwconv_plan_candidates: pass in {FWD, BWD_DATA, BWD_FILTER, BWD (fused backward, NCHW;
+ *     dwconv_bwd_workspace_bytes reflects its selection)}; NCHW and NHWC; writes at most
  *     max_candidates entries to infos (caller-owned array) and the number written
- *     to *count; max_candidates = 0 only reports the total in *count.  Non-NCHW
- *     layouts, N = 0 and the generic override report 0 candidates.
+ *     to *count; max_candidates = 0 only reports the total in *count.  N = 0, the
+ *     generic override and shapes only the generic kernels cover report 0 candidates.
  *   dwconv_plan_select: index into the same list; -1 restores the planner's pick.
  *     Returns DWCONV_ERR_BAD_DESCRIPTOR if the list was not queried first or the
  *     index is out of range.  Both are host-only calls (no launches) and

@@ -117,7 +117,7 @@ PlanKey plan_key(const Geom& g, int pass, const DevInfo& di) {
 // planner's own pick for the same geometry, pass and device.
 std::mutex g_sel_mu;
 std::map<PlanKey, Plan> g_selected;
-std::map<PlanKey, std::vector<ChunkPlan>> g_candidates;
+std::map<PlanKey, std::vector<Plan>> g_candidates;
 
 void make_plan(const Geom& g, int pass, const DevInfo& di, Plan* p) {
   static std::mutex mu;
@@ -370,12 +370,67 @@ int dwconv_workspace_init(void* workspace, size_t workspace_bytes, dwconv_stream
   return cuda_status(cudaMemsetAsync(workspace, 0, workspace_bytes, reinterpret_cast<cudaStream_t>(stream)));
 }
 
-static void fill_chunk_info(const ChunkPlan& c, dwconv_plan_info* info) {
+static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* info) {
   std::memset(info, 0, sizeof(*info));
-  info->variant = DWCONV_VARIANT_NCHW_CHUNK;
-  info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
-  info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
-  info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+  info->variant = p.variant;
+  if (pass == DWCONV_PASS_BWD && p.variant != DWCONV_VARIANT_NCHW_CHUNK) {  // two-call fallback
+    info->variant = DWCONV_VARIANT_NONE;
+    info->launches = 2;
+    return;
+  }
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) {
+    const ChunkPlan& c = p.chunk;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
+    info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
+    info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+  } else if (p.variant == DWCONV_VARIANT_NHWC_TMA) {
+    const dwk::NhwcTmaPlan& c = p.tma;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
+    info->work_units = c.ntiles; info->rows_per_band = c.TH; info->planes_per_chunk = c.TW;
+    if (pass == DWCONV_PASS_BWD_FILTER) {
+      info->work_units = (int64_t)c.ncb * c.tiles_per_cb;
+      info->batch_slices = c.nslices; info->max_chain = c.max_chain;
+      info->workspace_bytes = (int64_t)std::max(c.ws_bytes, p.nhwc.grid > 0 ? p.nhwc.ws_bytes : (size_t)0);
+    }
+  } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
+    const NhwcPlan& c = p.nhwc;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
+    info->work_units = (pass == DWCONV_PASS_BWD_FILTER) ? (int64_t)c.groups * c.nslices : c.items;
+    info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+  } else if (p.variant == DWCONV_VARIANT_GENERIC) {
+    info->block = 256; info->launches = 1;
+    if (pass == DWCONV_PASS_BWD_FILTER) {
+      info->grid = (int)(g.C * g.m * g.kh * g.kw);
+      const int64_t per = (g.N * g.Ho * g.Wo + 255) / 256;
+      info->max_chain = (int)(64 + 64 + per / 4096 + 2 + 8);
+    }
+  } else if (pass == DWCONV_PASS_BWD_FILTER) {
+    info->launches = 1;  // memset of dw
+  }
+}
+
+// NHWC candidates: the TMA family at several tile widths / ring depths, then the
+// L1 register-tile kernels.
+static void nhwc_candidates(const Geom& g, int pass, const DevInfo& di, std::vector<Plan>* cands) {
+  static const int shapes[][2] = {{16, 2}, {16, 3}, {16, 4}, {8, 2}, {8, 3}, {8, 4}, {4, 3}, {4, 4}, {32, 2}};
+  for (const auto& sh : shapes) {
+    Plan v;
+    v.variant = DWCONV_VARIANT_NHWC_TMA;
+    const bool ok = (pass == DWCONV_PASS_BWD_FILTER)
+                        ? dwk::plan_nhwc_tma_bf(g, di.sms, di.smem_optin, &v.tma, sh[0], sh[1])
+                        : dwk::plan_nhwc_tma(g, pass, di.sms, di.smem_optin, &v.tma, sh[0], sh[1]);
+    if (!ok) continue;
+    if (!dwk::plan_nhwc(g, pass, di.sms, &v.nhwc)) v.nhwc = NhwcPlan{};
+    bool dup = false;
+    for (const Plan& o : *cands)
+      dup = dup || (o.variant == v.variant && o.tma.TW == v.tma.TW && o.tma.ns == v.tma.ns && o.tma.grid == v.tma.grid);
+    if (!dup) cands->push_back(v);
+  }
+  Plan t;
+  if (dwk::plan_nhwc(g, pass, di.sms, &t.nhwc)) {
+    t.variant = DWCONV_VARIANT_NHWC_TILE;
+    cands->push_back(t);
+  }
 }
 
 int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, dwconv_plan_info* infos,
@@ -388,14 +443,41 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
   DevInfo di;
   if ((s = check_device(&di))) return s;
   *count = 0;
-  if (g.N == 0 || g.layout != DWCONV_NCHW || g_override.load() == DWCONV_VARIANT_GENERIC) return DWCONV_OK;
+  if (g.N == 0 || g_override.load() == DWCONV_VARIANT_GENERIC) return DWCONV_OK;
+  if (g.layout == DWCONV_NHWC && pass == DWCONV_PASS_BWD) return DWCONV_OK;
   const PlanKey key = plan_key(g, pass, di);
-  std::vector<ChunkPlan> cands;
+  std::vector<Plan> all;
   {
     std::lock_guard<std::mutex> lk(g_sel_mu);
     auto it = g_candidates.find(key);
-    if (it != g_candidates.end()) cands = it->second;
+    if (it != g_candidates.end()) all = it->second;
   }
+  if (all.empty() && g.layout == DWCONV_NHWC) {
+    Plan dp;
+    make_plan_uncached(g, pass, di, &dp);
+    if (dp.variant == DWCONV_VARIANT_NHWC_TMA || dp.variant == DWCONV_VARIANT_NHWC_TILE) {
+      all.push_back(dp);
+      nhwc_candidates(g, pass, di, &all);
+      // drop a later duplicate of the default
+      for (size_t i = 1; i < all.size(); ++i)
+        if (all[i].variant == dp.variant && all[i].tma.TW == dp.tma.TW && all[i].tma.ns == dp.tma.ns &&
+            all[i].tma.grid == dp.tma.grid && all[i].nhwc.grid == dp.nhwc.grid) {
+          all.erase(all.begin() + (long)i);
+          break;
+        }
+    }
+    if ((int)all.size() > DWCONV_MAX_CANDIDATES) all.resize(DWCONV_MAX_CANDIDATES);
+    std::lock_guard<std::mutex> lk(g_sel_mu);
+    g_candidates[key] = all;
+  }
+  if (g.layout == DWCONV_NHWC) {
+    const int n = std::min<int>((int)all.size(), max_candidates);
+    for (int i = 0; i < n; ++i) fill_info(g, all[i], pass, &infos[i]);
+    *count = (max_candidates == 0) ? (int)all.size() : n;
+    return DWCONV_OK;
+  }
+  std::vector<ChunkPlan> cands;
+  for (const Plan& q : all) cands.push_back(q.chunk);
   if (cands.empty()) {
     // the planner's own pick (what an unselected call launches) leads the list
     Plan dp;
@@ -442,11 +524,23 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         if (!dup) cands.push_back(c);
       }
     }
+    std::vector<Plan> wrapped;
+    for (const ChunkPlan& c : cands) {
+      Plan q;
+      q.variant = DWCONV_VARIANT_NCHW_CHUNK;
+      q.chunk = c;
+      wrapped.push_back(q);
+    }
     std::lock_guard<std::mutex> lk(g_sel_mu);
-    g_candidates[key] = cands;
+    g_candidates[key] = wrapped;
   }
   const int n = std::min<int>((int)cands.size(), max_candidates);
-  for (int i = 0; i < n; ++i) fill_chunk_info(cands[i], &infos[i]);
+  for (int i = 0; i < n; ++i) {
+    Plan q;
+    q.variant = DWCONV_VARIANT_NCHW_CHUNK;
+    q.chunk = cands[i];
+    fill_info(g, q, pass, &infos[i]);
+  }
   *count = (max_candidates == 0) ? (int)cands.size() : n;
   return DWCONV_OK;
 }
@@ -463,10 +557,7 @@ int dwconv_plan_select(const dwconv_desc* d, int pass, int index) {
   if (index < 0) { g_selected.erase(key); return DWCONV_OK; }
   auto it = g_candidates.find(key);
   if (it == g_candidates.end() || index >= (int)it->second.size()) return DWCONV_ERR_BAD_DESCRIPTOR;
-  Plan p;
-  p.variant = DWCONV_VARIANT_NCHW_CHUNK;
-  p.chunk = it->second[(size_t)index];
-  g_selected[key] = p;
+  g_selected[key] = it->second[(size_t)index];
   return DWCONV_OK;
 }
 
@@ -480,41 +571,7 @@ int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
   if ((s = check_device(&di))) return s;
   Plan p;
   make_plan(g, pass, di, &p);
-  std::memset(info, 0, sizeof(*info));
-  info->variant = p.variant;
-  if (pass == DWCONV_PASS_BWD && p.variant != DWCONV_VARIANT_NCHW_CHUNK) {  // two-call fallback
-    info->variant = DWCONV_VARIANT_NONE;
-    info->launches = 2;
-    return DWCONV_OK;
-  }
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK) {
-    const ChunkPlan& c = p.chunk;
-    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
-    info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
-    info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
-  } else if (p.variant == DWCONV_VARIANT_NHWC_TMA) {
-    const dwk::NhwcTmaPlan& c = p.tma;
-    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
-    info->work_units = c.ntiles; info->rows_per_band = c.TH; info->planes_per_chunk = c.TW;
-    if (pass == DWCONV_PASS_BWD_FILTER) {
-      info->work_units = (int64_t)c.ncb * c.tiles_per_cb;
-      info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
-    }
-  } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
-    const NhwcPlan& c = p.nhwc;
-    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
-    info->work_units = (pass == DWCONV_PASS_BWD_FILTER) ? (int64_t)c.groups * c.nslices : c.items;
-    info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
-  } else if (p.variant == DWCONV_VARIANT_GENERIC) {
-    info->block = 256; info->launches = 1;
-    if (pass == DWCONV_PASS_BWD_FILTER) {
-      info->grid = (int)(g.C * g.m * g.kh * g.kw);
-      const int64_t per = (g.N * g.Ho * g.Wo + 255) / 256;
-      info->max_chain = (int)(64 + 64 + per / 4096 + 2 + 8);
-    }
-  } else if (pass == DWCONV_PASS_BWD_FILTER) {
-    info->launches = 1;  // memset of dw
-  }
+  fill_info(g, p, pass, info);
   return DWCONV_OK;
 }
 

@@ -146,10 +146,13 @@ struct NhwcTmaPlan {
   int tiles_per_cb, nslices, tps, max_chain;
   size_t ws_bytes;
 };
-bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* plan);
+// tw_max / stages: tile-column cap and ring depth (0 = the defaults, env DWCONV_NHWC_TW / _STAGES)
+bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* plan, int tw_max = 0,
+                   int stages = 0);
 cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in, const void* w, void* out,
                             cudaStream_t st);
-bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* plan);
+bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* plan, int tw_max = 0,
+                      int stages = 0);
 cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* x, const void* dy, float* dw,
                                void* ws, cudaStream_t st);
 

@@ -502,7 +502,7 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 }  // namespace nhwct
 
 // Plan: mode, channel block, tile, box, ring depth, grid.  false = not eligible.
-bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* p) {
+bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* p, int tw_max, int stages) {
   using namespace nhwct;
   static const int on = env_int("DWCONV_NHWC_TMA", 1, 0, 1);
   if (!on || g.layout != DWCONV_NHWC || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
@@ -526,7 +526,8 @@ bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTma
   // divisor of the output width <= the CTA's thread budget)
   int TH = (OH % 7 == 0) ? 7 : 8;
   if (p->mode == kBd2) TH = (OH % 14 == 0) ? 14 : 8;
-  static const int tw_max_env = env_int("DWCONV_NHWC_TW", 16, 1, 64);
+  static const int tw_max_env0 = env_int("DWCONV_NHWC_TW", 16, 1, 64);
+  const int tw_max_env = tw_max > 0 ? tw_max : tw_max_env0;
   const int per_col = (p->mode == kBd2) ? 2 : 1;  // dx columns per consumer thread
   int tw_cap = std::min<int>(tw_max_env * per_col, (kMaxConsumers / NCV) * per_col);
   int TW = 0;
@@ -544,7 +545,8 @@ bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTma
   box_of(TW, &BW, &BH);
   // keep the ring of a CTA <= ~100 KB so two or more CTAs share an SM (stride-2
   // forward boxes are 4x the tile): narrower tiles, still dividing the width
-  static const int ns_want = env_int("DWCONV_NHWC_STAGES", 4, 2, 8);
+  static const int ns_env = env_int("DWCONV_NHWC_STAGES", 4, 2, 8);
+  const int ns_want = stages > 0 ? stages : ns_env;
   while ((int64_t)ns_want * CB * BW * BH * eb > 100 * 1024 && TW > 4) {
     int t = TW - 1;
     while (t > 4 && (OW % t != 0 || (p->mode == kBd2 && (t % 2)))) --t;
@@ -621,7 +623,7 @@ cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in,
   return cudaLaunchKernelEx(&cfg, fn, tm, a);
 }
 
-bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p) {
+bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p, int tw_max, int stages) {
   using namespace nhwct;
   static const int on = env_int("DWCONV_NHWC_TMA", 1, 0, 1);
   if (!on || g.layout != DWCONV_NHWC || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
@@ -638,13 +640,15 @@ bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p
   if (g.C % CB != 0 || (CB * eb) % 16 != 0) return false;
   const int NCV = (int)(CB / VC);
   const int TH = (g.Ho % 7 == 0) ? 7 : 8;
-  static const int tw_env = env_int("DWCONV_NHWC_TW", 16, 1, 64);
+  static const int tw_env0 = env_int("DWCONV_NHWC_TW", 16, 1, 64);
+  const int tw_env = tw_max > 0 ? tw_max : tw_env0;
   const int tw_cap = std::max(1, std::min(tw_env, kMaxConsumers / NCV));
   int TW = 0;
   for (int t = (int)std::min<int64_t>(g.Wo, tw_cap); t >= 1; --t)
     if (g.Wo % t == 0) { TW = t; break; }
   if (TW < tw_cap / 2 && g.Wo > tw_cap) TW = tw_cap;
-  static const int ns_want = env_int("DWCONV_NHWC_STAGES", 4, 2, 8);
+  static const int ns_env = env_int("DWCONV_NHWC_STAGES", 4, 2, 8);
+  const int ns_want = stages > 0 ? stages : ns_env;
   auto sizes = [&](int tw, int* bw, int* bh, uint32_t* xb, uint32_t* db) {
     *bw = (tw - 1) * S + 3; *bh = (TH - 1) * S + 3;
     *xb = (uint32_t)(CB * *bw * *bh * eb);

@@ -21,7 +21,7 @@ from typing import Dict, List, Optional
 import torch
 
 from . import ops
-from ._lib import NCHW, PASS_BWD, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_FWD
+from ._lib import PASS_BWD, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_FWD
 
 PASSES = {"fwd": PASS_FWD, "bwd_data": PASS_BWD_DATA, "bwd_filter": PASS_BWD_FILTER, "bwd": PASS_BWD}
 
@@ -49,20 +49,21 @@ def _graph_us(calls, reps: int, stream: torch.cuda.Stream) -> float:
 
 def tune_layer(d, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, passes=("fwd", "bwd_data", "bwd_filter"),
                reps: int = 3, min_gain: float = 0.02, stream: Optional[torch.cuda.Stream] = None) -> Dict[str, dict]:
-    """Select the fastest candidate plan of each pass for descriptor ``d`` (NCHW only).
+    """Select the fastest candidate plan of each pass for descriptor ``d`` (NCHW or NHWC).
 
     x, dy, w: the layer's tensors (their values are not modified).  Returns, per
     pass, the chosen index, its time and the default's time (microseconds).
     """
     out: Dict[str, dict] = {}
-    if d.layout != NCHW or d.n == 0:
+    if d.n == 0:
         return out
     dev = x.device
     stream = stream or torch.cuda.Stream(device=dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     set_bytes = sum(t.numel() * t.element_size() for t in (x, dy)) * 2
     nsets = int(max(2, min(8, -(-2 * l2 // set_bytes))))
-    sets = [dict(x=x, dy=dy)] + [dict(x=x.clone(), dy=dy.clone()) for _ in range(nsets - 1)]
+    sets = [dict(x=x, dy=dy)] + [dict(x=x.clone(memory_format=torch.preserve_format),
+                                      dy=dy.clone(memory_format=torch.preserve_format)) for _ in range(nsets - 1)]
     for s in sets:
         s["y"] = torch.empty_like(dy)
         s["dx"] = torch.empty_like(x)

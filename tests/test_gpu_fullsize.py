@@ -18,27 +18,28 @@ import torch
 import oracle
 import synth
 from paper_1803_09926_b200 import ops
-from paper_1803_09926_b200._lib import F32, BF16, NCHW
+from paper_1803_09926_b200._lib import F32, BF16, NCHW, NHWC
 
 pytestmark = pytest.mark.gpu
 
 NSAMP = 6
 
 
-def _dev(a, dtype):
+def _dev(a, dtype, layout=NCHW):
     t = torch.from_numpy(a)
-    return (t.to(torch.bfloat16) if dtype == "bf16" else t).cuda()
+    t = (t.to(torch.bfloat16) if dtype == "bf16" else t).cuda()
+    return t.contiguous(memory_format=torch.channels_last) if (layout == NHWC and t.dim() == 4) else t
 
 
-def _check_layer(L, dtype, amax, seed):
+def _check_layer(L, dtype, amax, seed, layout=NCHW):
     rng = np.random.default_rng(seed)
     x = synth.integers(seed * 10 + 1, (L.n, L.c, L.h, L.w), amax)
     w = synth.integers(seed * 10 + 2, (L.c * L.m, L.k, L.k), amax)
     dy = synth.integers(seed * 10 + 3, (L.n, L.c * L.m, L.ho, L.wo), amax)
-    d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, NCHW, F32 if dtype == "f32" else BF16)
-    xd, wd, dyd = _dev(x, dtype), _dev(w, dtype), _dev(dy, dtype)
-    y = torch.empty(dyd.shape, dtype=dyd.dtype, device="cuda")
-    dx = torch.empty(xd.shape, dtype=xd.dtype, device="cuda")
+    d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout, F32 if dtype == "f32" else BF16)
+    xd, wd, dyd = _dev(x, dtype, layout), _dev(w, dtype), _dev(dy, dtype, layout)
+    y = torch.empty_like(dyd)
+    dx = torch.empty_like(xd)
     dwt = torch.empty(w.shape, dtype=torch.float32, device="cuda")
     planes = [(int(rng.integers(L.n)), int(rng.integers(L.c))) for _ in range(NSAMP)]
     chans = sorted({int(c) for c in rng.integers(L.c, size=NSAMP)})
@@ -83,7 +84,7 @@ def _check_layer(L, dtype, amax, seed):
         finally:
             ops.dwconv_plan_select(d, pas, -1)
     # fused backward (dwconv_bwd: dx and dw from one pass) where the library has it
-    if ops.dwconv_plan(d, 3)["variant_name"] != "none":
+    if layout == NCHW and ops.dwconv_plan(d, 3)["variant_name"] != "none":
         cands = ops.dwconv_plan_candidates(d, 3)
         ws = torch.zeros(max(16, max(c["workspace_bytes"] for c in cands)), dtype=torch.uint8, device="cuda")
         try:
@@ -107,6 +108,14 @@ def _check_layer(L, dtype, amax, seed):
 def test_candidates_fullsize_b64_fp32(layer):
     L = [l for l in synth.mobilenet_v1_dw(64) if l.name == layer][0]
     _check_layer(L, "f32", 4, seed=7)
+
+
+@pytest.mark.parametrize("layer", ["dw2", "dw4", "dw8", "dw14", "dw24", "dw26"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_candidates_fullsize_nhwc(layer, dtype):
+    """NHWC: every TMA / register-tile candidate at the bench's sizes (b64 fp32, b128 bf16)."""
+    L = [l for l in synth.mobilenet_v1_dw(64 if dtype == "f32" else 128) if l.name == layer][0]
+    _check_layer(L, dtype, 4 if dtype == "f32" else 2, seed=9, layout=NHWC)
 
 
 @pytest.mark.parametrize("layer", ["dw2", "dw4", "dw14", "dw26"])
