@@ -498,14 +498,16 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     if (!cands.empty() && cands[0].small) {
       // other CTA sizes / ring depths of the small-plane kernel, then the chunk family's own pick
       // {warps, ring slots, batch slices (bwd_filter; 0 = about one wave)}
+      // (fwd / bwd_data: the third entry is tasks per warp instead)
       static const int shapes[][3] = {{2, 2, 0}, {2, 3, 0}, {4, 2, 0}, {8, 2, 0}, {8, 3, 0}, {8, 4, 0},
-                                      {8, 2, 1}, {8, 3, 1}, {8, 2, 2}, {4, 3, 2}};
+                                      {8, 2, 1}, {8, 3, 1}, {8, 2, 2}, {4, 3, 2}, {4, 2, 2}, {4, 2, 3},
+                                      {4, 3, 4}, {2, 2, 4}, {2, 3, 6}, {8, 2, 3}};
       for (const auto& sh : shapes) {
-        if (sh[2] && pass < DWCONV_PASS_BWD_FILTER) continue;
         ChunkPlan v;
         if (!dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2])) continue;
         bool dup = false;
-        for (const ChunkPlan& o : cands) dup = dup || (o.small && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices);
+        for (const ChunkPlan& o : cands)
+          dup = dup || (o.small && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices && o.grid == v.grid);
         if (!dup) cands.push_back(v);
       }
       if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch) &&

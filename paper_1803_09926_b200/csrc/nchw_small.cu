@@ -708,6 +708,11 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   if (!bf) {
     p->ntasks = g.N * g.C / 4;
     p->grid = (int)std::min<int64_t>((p->ntasks + p->warps - 1) / p->warps, (int64_t)occ * num_sms);
+    if (slices > 0) {  // fwd / bwd_data: `slices` = tasks per warp (an even split: no partial last round)
+      const int64_t g2 = (p->ntasks + (int64_t)p->warps * slices - 1) / ((int64_t)p->warps * slices);
+      if (g2 > (int64_t)occ * num_sms) return false;
+      p->grid = (int)g2;
+    }
     p->max_chain = 9;
     return true;
   }
