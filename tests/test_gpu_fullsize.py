@@ -55,13 +55,18 @@ def _check_layer(L, dtype, amax, seed, layout=NCHW):
                                                  (1, L.k, L.k), s, p)[0][0]
     for name, pas in (("fwd", 0), ("bwd_data", 1), ("bwd_filter", 2)):
         cands = ops.dwconv_plan_candidates(d, pas)
-        assert cands, f"{L.name} {name}: no NCHW candidates"
+        if not cands:  # shapes only the generic kernels cover: check the default path once
+            assert layout == NHWC or L.c < 4 or L.n == 0, f"{L.name} {name}: no candidates"
+            cands = [None]
         ws = None
         if pas == 2:
-            ws = torch.zeros(max(16, max(c["workspace_bytes"] for c in cands)), dtype=torch.uint8, device="cuda")
+            ws = torch.zeros(max(16, ops.dwconv_bwd_filter_workspace_bytes(d),
+                                 max((c["workspace_bytes"] for c in cands if c), default=0)),
+                             dtype=torch.uint8, device="cuda")
         try:
             for i, cand in enumerate(cands):
-                ops.dwconv_plan_select(d, pas, i)
+                if cand is not None:
+                    ops.dwconv_plan_select(d, pas, i)
                 tag = f"{L.name} {dtype} {name} candidate {i} {cand}"
                 if pas == 0:
                     y.fill_(float("nan"))
@@ -141,3 +146,23 @@ def test_tune_layer_selects_a_candidate():
     finally:
         for p in range(3):
             ops.dwconv_plan_select(d, p, -1)
+
+
+# Edge shapes for the small-plane / band / TMA candidates at small batch: one
+# channel group, channel counts that do not fill a CTA, single-image slices,
+# stride 2 on 14 / 28 planes, and the band kernel's one- and two-plane warps.
+EDGE = [
+    # (N, C, H, s)
+    (1, 4, 14, 1), (3, 12, 14, 1), (2, 8, 28, 1), (5, 4, 7, 1), (2, 20, 7, 1),
+    (3, 8, 14, 2), (2, 12, 28, 2),
+    (2, 6, 56, 1), (1, 3, 112, 1), (2, 4, 112, 2), (3, 5, 56, 2), (2, 2, 28, 1),
+]
+
+
+@pytest.mark.parametrize("layout", [NCHW, NHWC])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", EDGE)
+def test_candidates_edge_shapes(shape, dtype, layout):
+    n, c, h, s = shape
+    L = synth.Layer(name=f"edge{n}x{c}x{h}s{s}", n=n, c=c, h=h, w=h, k=3, s=s, p=1, m=1)
+    _check_layer(L, dtype, 3 if dtype == "f32" else 2, seed=11, layout=layout)
