@@ -495,6 +495,14 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     }
     std::vector<ChunkPlan> more;
     ChunkPlan scratch;
+    if (g.dtype == DWCONV_BF16 && pass <= DWCONV_PASS_BWD_DATA) {
+      // bf16 plane-pair small-plane kernels: {warps, ring slots}
+      static const int pshapes[][2] = {{4, 2}, {4, 3}, {8, 2}, {2, 3}, {2, 2}};
+      for (const auto& sh : pshapes) {
+        ChunkPlan v;
+        if (dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1], 0, true)) cands.push_back(v);
+      }
+    }
     if (!cands.empty() && cands[0].small) {
       // other CTA sizes / ring depths of the small-plane kernel, then the chunk family's own pick
       // {warps, ring slots, batch slices (bwd_filter; 0 = about one wave)}
@@ -507,7 +515,8 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         if (!dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2])) continue;
         bool dup = false;
         for (const ChunkPlan& o : cands)
-          dup = dup || (o.small && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices && o.grid == v.grid);
+          dup = dup || (o.small && !o.sp.pair && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices &&
+                        o.grid == v.grid);
         if (!dup) cands.push_back(v);
       }
       if (dwk::plan_nchw(g, pass, di.sms, di.smem_optin, &scratch) &&

@@ -43,6 +43,7 @@ struct SmallPlan {
   int groups, nslices, nps, max_chain;
   size_t ws_bytes;
   int S;  // stride of the small-plane kernels
+  bool pair;  // bf16 plane-pair kernel (8-plane tasks, FFMA2 over plane pairs)
   int occ, sms;  // resident CTAs per SM, SMs (early PDL only when the grid is one wave)
   // band bwd_filter for large planes (band_bf_kernel)
   bool band;
@@ -53,7 +54,7 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* pl
 // warps / stages: CTA size and per-warp ring depth (0 = the defaults, env DWCONV_SMALL_WARPS / _STAGES)
 // slices (bwd_filter): batch slices per channel group (0 = about one wave of CTAs)
 bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* plan, int warps = 0,
-                     int stages = 0, int slices = 0);
+                     int stages = 0, int slices = 0, bool pair = false);
 cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const void* in, const void* in2,
                               const void* w, void* out, float* dw, void* ws, cudaStream_t st);
 
@@ -104,7 +105,7 @@ constexpr int kPassBwdFused = DWCONV_PASS_BWD;  // plan_nchw pass id of the fuse
 bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* plan,
                std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
 bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps = 0,
-                      int stages = 0, int slices = 0);
+                      int stages = 0, int slices = 0, bool pair = false);
 bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* plan, int warps, int stages, int rows,
                      int ppw = 1);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,

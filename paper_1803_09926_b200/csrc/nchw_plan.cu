@@ -591,16 +591,16 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
 
 // A ChunkPlan that runs the small-plane warp-task kernels (nchw_small.cu).
 bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages,
-                      int slices) {
+                      int slices, bool pair) {
   SmallPlan sp;
-  if (!plan_nchw_small(g, pass, num_sms, smem_optin, &sp, warps, stages, slices)) return false;
+  if (!plan_nchw_small(g, pass, num_sms, smem_optin, &sp, warps, stages, slices, pair)) return false;
   *p = ChunkPlan{};
   p->small = true;
   p->sp = sp;
   p->threads = 32 * sp.warps;
   p->grid = sp.grid;
   p->smem_bytes = sp.smem;
-  p->P = 4;
+  p->P = sp.pair ? 8 : 4;
   p->nbands = 1;
   p->band_rows = (int)g.H;
   p->ns = sp.ns;

@@ -437,6 +437,102 @@ __device__ __forceinline__ void load_row2(const T* row, int c0, float* xv) {  //
   xv[0] = (c0 > 0) ? Elem<T>::load(row + 2 * c0 - 1) : 0.f;
 }
 
+// bf16 plane pairs (stride 1): a warp task is 8 planes; lane (p, column group)
+// owns planes p and p + 4 and runs their stencils together with packed FFMA2
+// (lanes of the float2 = the two planes), halving the FMA instructions per
+// output of the bf16 kernels, which are instruction-bound.
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
+  using T = __nv_bfloat16;
+  constexpr int V = W / 7, HW = W * W;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = lane / 7, cg = lane - pl * 7;
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const T* __restrict__ in = static_cast<const T*>(a.in);
+  T* __restrict__ out = static_cast<T*>(a.out);
+  const T* __restrict__ wt = static_cast<const T*>(a.w);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * nwarps;
+  const uint32_t task_bytes = 8u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int64_t t, int s) {
+    if (lane == 0 && t < a.ntasks) {
+      mbar_arrive_expect_tx(&bars[s], task_bytes);
+      bulk_g2s(slot(s), in + t * 8 * HW, task_bytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  if (a.early_pdl) griddep_launch_dependents();
+  const bool lft = c0 > 0, rgt = c0 + V < W;
+  auto ldrow = [&](const T* ra, const T* rb, float2* xv) {  // .x plane A, .y plane B
+    float va[V], vb[V];
+    VecIO<T, V>::load(ra + c0, va);
+    VecIO<T, V>::load(rb + c0, vb);
+#pragma unroll
+    for (int u = 0; u < V; ++u) xv[1 + u] = make_float2(va[u], vb[u]);
+    xv[0] = lft ? make_float2(Elem<T>::load(ra + c0 - 1), Elem<T>::load(rb + c0 - 1)) : make_float2(0.f, 0.f);
+    xv[V + 1] = rgt ? make_float2(Elem<T>::load(ra + c0 + V), Elem<T>::load(rb + c0 + V)) : make_float2(0.f, 0.f);
+  };
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = gw; t < a.ntasks; t += stride) {
+    const int64_t qa = t * 8 + pl, qb = qa + 4;
+    const int ca = (int)(qa % a.C), cb2 = (int)(qb % a.C);
+    float2 w2[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int kk = (MODE == 1) ? 8 - k : k;
+      w2[k] = make_float2(Elem<T>::ldg(wt + (int64_t)ca * 9 + kk), Elem<T>::ldg(wt + (int64_t)cb2 * 9 + kk));
+    }
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      const T* pa = slot(s) + pl * HW;
+      const T* pb = pa + 4 * HW;
+      float2 xw[3][V + 2];
+#pragma unroll
+      for (int u = 0; u < V + 2; ++u) xw[0][u] = make_float2(0.f, 0.f);
+      ldrow(pa, pb, xw[1]);
+      T* poa = out + qa * HW + c0;
+      T* pob = out + qb * HW + c0;
+#pragma unroll
+      for (int r = 0; r < W; ++r) {
+        if (r + 1 < W) ldrow(pa + (r + 1) * W, pb + (r + 1) * W, xw[2]);
+        else
+#pragma unroll
+          for (int u = 0; u < V + 2; ++u) xw[2][u] = make_float2(0.f, 0.f);
+        float oa[V], ob[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          float2 acc = __fmul2_rn(w2[0], xw[0][u]);
+#pragma unroll
+          for (int k = 1; k < 9; ++k) acc = __ffma2_rn(w2[k], xw[k / 3][u + k % 3], acc);
+          oa[u] = acc.x;
+          ob[u] = acc.y;
+        }
+        VecIO<T, V>::store(poa + r * W, oa);
+        VecIO<T, V>::store(pob + r * W, ob);
+#pragma unroll
+        for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
+      }
+    }
+    __syncwarp();
+    issue(t + a.ns * stride, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  if (!a.early_pdl) griddep_launch_dependents();
+}
+
 template <class T, int W>
 __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
   constexpr int Wo = W / 2, V = Wo / 7, HW = W * W, HWo = Wo * Wo, NXW = 2 * V + 1;
@@ -653,6 +749,13 @@ SKernelFn pick2(int pass, int W) {  // stride 2: fwd and bwd_filter
   if (pass == 2) return W == 14 ? small_bf2_kernel<T, 14> : W == 28 ? small_bf2_kernel<T, 28> : nullptr;
   return nullptr;
 }
+SKernelFn pair_kernel_for(int pass, int W) {
+  if (pass == 0) return W == 7 ? small_fd_pair_kernel<7, 0> : W == 14 ? small_fd_pair_kernel<14, 0>
+                      : W == 28 ? small_fd_pair_kernel<28, 0> : nullptr;
+  if (pass == 1) return W == 7 ? small_fd_pair_kernel<7, 1> : W == 14 ? small_fd_pair_kernel<14, 1>
+                      : W == 28 ? small_fd_pair_kernel<28, 1> : nullptr;
+  return nullptr;
+}
 SKernelFn kernel_for(int dtype, int pass, int W, int S = 1) {
   if (S == 2) return dtype == DWCONV_F32 ? pick2<float>(pass, W) : pick2<__nv_bfloat16>(pass, W);
   return dtype == DWCONV_F32 ? pick<float>(pass, W) : pick<__nv_bfloat16>(pass, W);
@@ -668,7 +771,7 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 
 // Eligibility + launch shape.  pass: 0 fwd, 1 bwd_data, 2 bwd_filter.
 bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages,
-                     int slices) {
+                     int slices, bool pair) {
   using namespace small;
   static const int on = env_int("DWCONV_SMALL", 1, 0, 1);
   if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
@@ -679,7 +782,8 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   if (S != 1 && S != 2) return false;
   if (g.C % 4 != 0 || g.N < 1) return false;
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
-  const int64_t task_bytes = 4 * g.H * g.W * eb;
+  if (pair && (g.dtype != DWCONV_BF16 || S != 1 || pass > 1 || (g.N * g.C) % 8 != 0)) return false;
+  const int64_t task_bytes = (pair ? 8 : 4) * g.H * g.W * eb;
   const int64_t dy_bytes = 4 * g.Ho * g.Wo * eb;
   if (task_bytes % 16 != 0 || (pass >= 2 && dy_bytes % 16 != 0)) return false;  // bulk copies: 16-B granules
   *p = SmallPlan{};
@@ -690,10 +794,11 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   const bool bf = pass >= 2;  // bwd_filter or the fused backward
   p->slot_bytes = (uint32_t)(task_bytes + (bf ? dy_bytes : 0));
   p->S = S;
+  p->pair = pair;
   p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
   if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * 9 * 4);
   if (p->smem > smem_optin - 1024) return false;
-  SKernelFn fn = kernel_for(g.dtype, pass, (int)g.W, S);
+  SKernelFn fn = pair ? pair_kernel_for(pass, (int)g.W) : kernel_for(g.dtype, pass, (int)g.W, S);
   if (!fn) return false;
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
@@ -706,7 +811,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   p->occ = occ;
   p->sms = num_sms;
   if (!bf) {
-    p->ntasks = g.N * g.C / 4;
+    p->ntasks = g.N * g.C / (pair ? 8 : 4);
     p->grid = (int)std::min<int64_t>((p->ntasks + p->warps - 1) / p->warps, (int64_t)occ * num_sms);
     if (slices > 0) {  // fwd / bwd_data: `slices` = tasks per warp (an even split: no partial last round)
       const int64_t g2 = (p->ntasks + (int64_t)p->warps * slices - 1) / ((int64_t)p->warps * slices);
@@ -810,7 +915,8 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   }
-  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R, p.ppw) : kernel_for(g.dtype, pass, (int)g.W, p.S);
+  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R, p.ppw)
+               : p.pair ? pair_kernel_for(pass, (int)g.W) : kernel_for(g.dtype, pass, (int)g.W, p.S);
   if (!fn) return cudaErrorInvalidValue;
   static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
   cudaLaunchConfig_t cfg = {};
