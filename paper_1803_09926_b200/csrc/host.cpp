@@ -495,7 +495,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     }
     std::vector<ChunkPlan> more;
     ChunkPlan scratch;
-    if (g.dtype == DWCONV_BF16 && pass <= DWCONV_PASS_BWD_DATA) {
+    if (g.dtype == DWCONV_BF16 && pass <= DWCONV_PASS_BWD_FILTER) {
       // bf16 plane-pair small-plane kernels: {warps, ring slots}
       static const int pshapes[][2] = {{4, 2}, {4, 3}, {8, 2}, {2, 3}, {2, 2}};
       for (const auto& sh : pshapes) {

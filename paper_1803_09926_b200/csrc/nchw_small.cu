@@ -533,6 +533,133 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
   if (!a.early_pdl) griddep_launch_dependents();
 }
 
+// bf16 plane-pair bwd_filter (stride 1): CTA = (group of 8 channels, batch
+// slice); lane (p, column group) owns channels cb + p and cb + p + 4 and
+// accumulates both with FFMA2 (float2 lanes = the two channels).  Reduction as
+// small_bf_kernel, per channel.
+template <int W>
+__global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
+  using T = __nv_bfloat16;
+  constexpr int V = W / 7, HW = W * W;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = lane / 7, cg = lane - pl * 7;
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
+  const int cb = g * 8;
+  const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const uint32_t task_bytes = 8u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int n, int s) {
+    if (lane == 0 && n < n1) {
+      const int64_t off = ((int64_t)n * a.C + cb) * HW;
+      mbar_arrive_expect_tx(&bars[s], 2 * task_bytes);
+      bulk_g2s(slot(s), x + off, task_bytes, &bars[s]);
+      bulk_g2s(slot(s) + 8 * HW, dy + off, task_bytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
+  if (a.early_pdl) griddep_launch_dependents();
+  const bool lft = c0 > 0, rgt = c0 + V < W;
+  auto ldrow = [&](const T* ra, const T* rb, float2* xv) {
+    float va[V], vb[V];
+    VecIO<T, V>::load(ra + c0, va);
+    VecIO<T, V>::load(rb + c0, vb);
+#pragma unroll
+    for (int u = 0; u < V; ++u) xv[1 + u] = make_float2(va[u], vb[u]);
+    xv[0] = lft ? make_float2(Elem<T>::load(ra + c0 - 1), Elem<T>::load(rb + c0 - 1)) : make_float2(0.f, 0.f);
+    xv[V + 1] = rgt ? make_float2(Elem<T>::load(ra + c0 + V), Elem<T>::load(rb + c0 + V)) : make_float2(0.f, 0.f);
+  };
+  float2 run[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) run[k] = make_float2(0.f, 0.f);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int n = n0 + warp; n < n1; n += nwarps) {
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      const T* pa = slot(s) + pl * HW;
+      const T* pb = pa + 4 * HW;
+      const T* da = slot(s) + 8 * HW + pl * HW;
+      const T* db = da + 4 * HW;
+      float2 xw[3][V + 2];
+#pragma unroll
+      for (int u = 0; u < V + 2; ++u) xw[0][u] = make_float2(0.f, 0.f);
+      ldrow(pa, pb, xw[1]);
+      float2 loc[9];
+#pragma unroll
+      for (int r = 0; r < W; ++r) {
+        if (r + 1 < W) ldrow(pa + (r + 1) * W, pb + (r + 1) * W, xw[2]);
+        else
+#pragma unroll
+          for (int u = 0; u < V + 2; ++u) xw[2][u] = make_float2(0.f, 0.f);
+        float dva[V], dvb[V];
+        VecIO<T, V>::load(da + r * W + c0, dva);
+        VecIO<T, V>::load(db + r * W + c0, dvb);
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            const float2 dv = make_float2(dva[u], dvb[u]);
+            loc[k] = (r == 0 && u == 0) ? __fmul2_rn(xw[k / 3][u + k % 3], dv)
+                                        : __ffma2_rn(xw[k / 3][u + k % 3], dv, loc[k]);
+          }
+#pragma unroll
+        for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) run[k] = __fadd2_rn(run[k], loc[k]);
+    }
+    __syncwarp();
+    issue(n + a.ns * nwarps, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  if (!a.early_pdl) griddep_launch_dependents();
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem + 64 * nwarps);  // [warp][lane][18]; the ring is idle now
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      red[(warp * 32 + lane) * 18 + k] = run[k].x;
+      red[(warp * 32 + lane) * 18 + 9 + k] = run[k].y;
+    }
+  }
+  __syncthreads();
+  float* part = a.ws_part + (int64_t)sl * a.C * 9;
+  for (int e = threadIdx.x; e < 8 * 9; e += blockDim.x) {
+    const int ch = e / 9, k = e - ch * 9;  // channel cb + ch
+    const int p = ch & 3, hi = ch >> 2;
+    float tot = 0.f;
+    for (int wv = 0; wv < nwarps; ++wv) {
+      float v = red[(wv * 32 + p * 7) * 18 + hi * 9 + k];
+      for (int l = 1; l < 7; ++l) v += red[(wv * 32 + p * 7 + l) * 18 + hi * 9 + k];
+      tot = (wv == 0) ? v : tot + v;
+    }
+    part[(int64_t)(cb + ch) * 9 + k] = tot;
+  }
+  __threadfence();
+  __syncthreads();
+  {
+    const int ngrp = (a.nslices + 31) / 32;
+    nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
+                             a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
+                             (int64_t)cb * 9, 72, a.dw, &s_last);
+  }
+}
+
 template <class T, int W>
 __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
   constexpr int Wo = W / 2, V = Wo / 7, HW = W * W, HWo = Wo * Wo, NXW = 2 * V + 1;
@@ -750,6 +877,8 @@ SKernelFn pick2(int pass, int W) {  // stride 2: fwd and bwd_filter
   return nullptr;
 }
 SKernelFn pair_kernel_for(int pass, int W) {
+  if (pass == 2) return W == 7 ? small_bf_pair_kernel<7> : W == 14 ? small_bf_pair_kernel<14>
+                      : W == 28 ? small_bf_pair_kernel<28> : nullptr;
   if (pass == 0) return W == 7 ? small_fd_pair_kernel<7, 0> : W == 14 ? small_fd_pair_kernel<14, 0>
                       : W == 28 ? small_fd_pair_kernel<28, 0> : nullptr;
   if (pass == 1) return W == 7 ? small_fd_pair_kernel<7, 1> : W == 14 ? small_fd_pair_kernel<14, 1>
@@ -782,9 +911,9 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   if (S != 1 && S != 2) return false;
   if (g.C % 4 != 0 || g.N < 1) return false;
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
-  if (pair && (g.dtype != DWCONV_BF16 || S != 1 || pass > 1 || (g.N * g.C) % 8 != 0)) return false;
+  if (pair && (g.dtype != DWCONV_BF16 || S != 1 || pass > 2 || (g.N * g.C) % 8 != 0 || (pass == 2 && g.C % 8))) return false;
   const int64_t task_bytes = (pair ? 8 : 4) * g.H * g.W * eb;
-  const int64_t dy_bytes = 4 * g.Ho * g.Wo * eb;
+  const int64_t dy_bytes = (pair ? 8 : 4) * g.Ho * g.Wo * eb;
   if (task_bytes % 16 != 0 || (pass >= 2 && dy_bytes % 16 != 0)) return false;  // bulk copies: 16-B granules
   *p = SmallPlan{};
   static const int warps_env = env_int("DWCONV_SMALL_WARPS", 4, 1, 8);
@@ -796,7 +925,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   p->S = S;
   p->pair = pair;
   p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
-  if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * 9 * 4);
+  if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * (pair ? 18 : 9) * 4);
   if (p->smem > smem_optin - 1024) return false;
   SKernelFn fn = pair ? pair_kernel_for(pass, (int)g.W) : kernel_for(g.dtype, pass, (int)g.W, S);
   if (!fn) return false;
@@ -821,8 +950,8 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
     p->max_chain = 9;
     return true;
   }
-  // bwd_filter: groups of 4 channels x batch slices, ~one wave, <= 32 images per warp
-  p->groups = (int)(g.C / 4);
+  // bwd_filter: groups of 4 (pair: 8) channels x batch slices, ~one wave, <= 32 images per warp
+  p->groups = (int)(g.C / (pair ? 8 : 4));
   int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
   nsl = std::max<int64_t>(nsl, (g.N + 32 * p->warps - 1) / (32 * p->warps));
   nsl = std::min<int64_t>(nsl, std::min<int64_t>(g.N, 128));
