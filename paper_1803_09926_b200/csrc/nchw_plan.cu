@@ -623,7 +623,7 @@ bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* p, i
   p->threads = 32 * sp.warps;
   p->grid = sp.grid;
   p->smem_bytes = sp.smem;
-  p->P = sp.ppw;
+  p->P = (sp.ppw == 1) ? 1 : 2;
   p->nbands = sp.nbands;
   p->band_rows = sp.R;
   p->ns = sp.ns;

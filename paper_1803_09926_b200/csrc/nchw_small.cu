@@ -836,6 +836,157 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   }
 }
 
+// Band bwd_filter over channel PAIRS: every lane owns V dy columns of two
+// consecutive channels (the task stages both planes' bands) and accumulates
+// them as packed FFMA2 (float2 lanes = the two channels) -- half the FMA
+// instructions of band_bf_kernel, for the instruction-bound bf16 case.
+template <class T, int S, int V, int R>
+__global__ void __launch_bounds__(256) band_bf_pair_kernel(const SArgs a) {
+  constexpr int NX = S * V;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
+  const int cw = g * a.cpg + warp * 2;  // channels cw, cw + 1
+  const int np_w = max(0, min(2, min(a.cpg - warp * 2, a.C - cw)));
+  const bool wlive = np_w > 0;
+  const int H = a.H, W = a.W, Ho = a.Ho, Wo = a.Wo;
+  const bool live = wlive && lane * V < Wo;
+  const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
+  const int ntask = (n1 - n0) * a.nbands;
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  const uint32_t xcap = (uint32_t)(((R - 1) * S + 3) * W * sizeof(T) + 15) & ~15u;
+  const uint32_t dcap = (uint32_t)(R * Wo * sizeof(T) + 15) & ~15u;
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  auto slot = [&](int s) { return reinterpret_cast<unsigned char*>(ring) + (size_t)s * a.slot_bytes; };
+  auto rows_of = [&](int t, int* n, int* r0, int* r1, int* lo, int* hi) {
+    const int nn = t / a.nbands, b = t - nn * a.nbands;
+    *n = n0 + nn;
+    *r0 = b * R;
+    *r1 = min(*r0 + R, Ho);
+    *lo = max(0, *r0 * S - 1);
+    *hi = min(H, (*r1 - 1) * S + 2);
+  };
+  auto issue = [&](int t, int s) {
+    if (lane == 0 && wlive && t < ntask) {
+      int n, r0, r1, lo, hi;
+      rows_of(t, &n, &r0, &r1, &lo, &hi);
+      const uint32_t xb = (uint32_t)((hi - lo) * W * sizeof(T)), db = (uint32_t)((r1 - r0) * Wo * sizeof(T));
+      mbar_arrive_expect_tx(&bars[s], (uint32_t)np_w * (xb + db));
+      for (int p = 0; p < np_w; ++p) {
+        unsigned char* sp = slot(s) + (size_t)p * (xcap + dcap);
+        bulk_g2s(sp, x + (((int64_t)n * a.C + cw + p) * H + lo) * W, xb, &bars[s]);
+        bulk_g2s(sp + xcap, dy + (((int64_t)n * a.C + cw + p) * Ho + r0) * Wo, db, &bars[s]);
+      }
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(i, i);
+  if (a.early_pdl) griddep_launch_dependents();
+  const int c0 = lane * V;
+  float2 run[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) run[k] = make_float2(0.f, 0.f);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int t = 0; t < (wlive ? ntask : 0); ++t) {
+    mbar_wait(&bars[s], ph);
+    if (live) {
+      int n, r0, r1, lo, hi;
+      rows_of(t, &n, &r0, &r1, &lo, &hi);
+      const unsigned char* spa = slot(s);
+      const unsigned char* spb = slot(s) + (np_w > 1 ? (xcap + dcap) : 0);  // a lone last channel pairs with itself
+      const T* xa = reinterpret_cast<const T*>(spa) - (int64_t)lo * W;
+      const T* xb2 = reinterpret_cast<const T*>(spb) - (int64_t)lo * W;
+      const T* dsa = reinterpret_cast<const T*>(spa + xcap) - (int64_t)r0 * Wo;
+      const T* dsb = reinterpret_cast<const T*>(spb + xcap) - (int64_t)r0 * Wo;
+      float2 xw[3][NX + 2];
+      auto ldx = [&](int ih, float2* v) {
+        if (ih >= lo && ih < hi) {
+          const T* ra = xa + (int64_t)ih * W;
+          const T* rb = xb2 + (int64_t)ih * W;
+          float oa[NX], ob[NX];
+          VecIO<T, NX>::load(ra + S * c0, oa);
+          VecIO<T, NX>::load(rb + S * c0, ob);
+#pragma unroll
+          for (int u = 0; u < NX; ++u) v[1 + u] = make_float2(oa[u], ob[u]);
+          v[0] = (c0 > 0) ? make_float2(Elem<T>::load(ra + S * c0 - 1), Elem<T>::load(rb + S * c0 - 1))
+                          : make_float2(0.f, 0.f);
+          v[NX + 1] = (S == 1 && c0 + V < W) ? make_float2(Elem<T>::load(ra + c0 + V), Elem<T>::load(rb + c0 + V))
+                                             : make_float2(0.f, 0.f);
+        } else {
+#pragma unroll
+          for (int u = 0; u < NX + 2; ++u) v[u] = make_float2(0.f, 0.f);
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < 3 - S; ++i) ldx(r0 * S - 1 + i, xw[i]);
+      float2 loc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) loc[k] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const int r = r0 + rr;
+        if (r < r1) {
+#pragma unroll
+          for (int i = 3 - S; i < 3; ++i) ldx(r * S - 1 + i, xw[i]);
+          float da[V], db[V];
+          VecIO<T, V>::load(dsa + (int64_t)r * Wo + c0, da);
+          VecIO<T, V>::load(dsb + (int64_t)r * Wo + c0, db);
+#pragma unroll
+          for (int k = 0; k < 9; ++k)
+#pragma unroll
+            for (int u = 0; u < V; ++u)
+              loc[k] = __ffma2_rn(xw[k / 3][S * u + k % 3], make_float2(da[u], db[u]), loc[k]);
+#pragma unroll
+          for (int i = 0; i < 3 - S; ++i)
+#pragma unroll
+            for (int u = 0; u < NX + 2; ++u) xw[i][u] = xw[i + S][u];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) run[k] = __fadd2_rn(run[k], loc[k]);
+    }
+    __syncwarp();
+    issue(t + a.ns, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  if (!a.early_pdl) griddep_launch_dependents();
+  // ---- lanes: fixed xor tree per channel -> the warp's two channel partials
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      run[k].x += __shfl_xor_sync(0xffffffffu, run[k].x, off);
+      run[k].y += __shfl_xor_sync(0xffffffffu, run[k].y, off);
+    }
+  }
+  float* part = a.ws_part + (int64_t)sl * a.C * 9;
+  if (lane < 9 * np_w) {
+    const int p = lane / 9, kk = lane - p * 9;
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v = (kk == k) ? (p ? run[k].y : run[k].x) : v;
+    part[(int64_t)(cw + p) * 9 + kk] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  {
+    const int ngrp = (a.nslices + 31) / 32;
+    nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
+                             a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
+                             (int64_t)g * a.cpg * 9, min(a.cpg, a.C - g * a.cpg) * 9, a.dw, &s_last);
+  }
+}
+
 using SKernelFn = void (*)(SArgs);
 
 template <class T, int S, int R, int PPW>
@@ -852,7 +1003,20 @@ SKernelFn band_pick_sr(int S, int V, int R) {
   if (S == 1) return R == 7 ? band_pick_v<T, 1, 7, PPW>(V) : band_pick_v<T, 1, 14, PPW>(V);
   return R == 7 ? band_pick_v<T, 2, 7, PPW>(V) : band_pick_v<T, 2, 14, PPW>(V);
 }
+template <class T>
+SKernelFn band_pair_pick(int S, int V, int R) {
+  if (S == 1) {
+    if (V == 1) return R == 7 ? band_bf_pair_kernel<T, 1, 1, 7> : band_bf_pair_kernel<T, 1, 1, 14>;
+    if (V == 2) return R == 7 ? band_bf_pair_kernel<T, 1, 2, 7> : band_bf_pair_kernel<T, 1, 2, 14>;
+    if (V == 4) return R == 7 ? band_bf_pair_kernel<T, 1, 4, 7> : band_bf_pair_kernel<T, 1, 4, 14>;
+  } else {
+    if (V == 1) return R == 7 ? band_bf_pair_kernel<T, 2, 1, 7> : band_bf_pair_kernel<T, 2, 1, 14>;
+    if (V == 2) return R == 7 ? band_bf_pair_kernel<T, 2, 2, 7> : band_bf_pair_kernel<T, 2, 2, 14>;
+  }
+  return nullptr;
+}
 SKernelFn band_kernel_for(int dtype, int S, int V, int R, int PPW = 1) {
+  if (PPW == 3) return dtype == DWCONV_F32 ? band_pair_pick<float>(S, V, R) : band_pair_pick<__nv_bfloat16>(S, V, R);
   if (dtype == DWCONV_F32) return PPW == 2 ? band_pick_sr<float, 2>(S, V, R) : band_pick_sr<float, 1>(S, V, R);
   using B = __nv_bfloat16;
   return PPW == 2 ? band_pick_sr<B, 2>(S, V, R) : band_pick_sr<B, 1>(S, V, R);
@@ -976,8 +1140,8 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   static const int on = env_int("DWCONV_BAND_BF", 1, 0, 1);
   if (!on || g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
   const int S = g.sh;
-  if (ppw != 1 && ppw != 2) return false;
-  const int lanes = 28 / ppw;  // output columns are split over 28 (one plane) or 14 (two planes) lanes
+  if (ppw != 1 && ppw != 2 && ppw != 3) return false;
+  const int lanes = (ppw == 2) ? 14 : 28;  // columns over 28 lanes (one plane / a channel pair) or 14 (two planes)
   if (g.sw != S || (S != 1 && S != 2) || g.Wo % lanes != 0 || g.W != S * g.Wo || g.N < 1) return false;
   const int V = (int)(g.Wo / lanes);
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
@@ -993,7 +1157,7 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   p->warps = warps;
   p->ns = stages;
   const int64_t xcap = ((((int64_t)rows - 1) * S + 3) * g.W * eb + 15) & ~(int64_t)15;
-  p->slot_bytes = (uint32_t)(ppw * (xcap + (((int64_t)rows * g.Wo * eb + 15) & ~(int64_t)15)));
+  p->slot_bytes = (uint32_t)((ppw == 1 ? 1 : 2) * (xcap + (((int64_t)rows * g.Wo * eb + 15) & ~(int64_t)15)));
   p->smem = 64 * warps + warps * stages * (int)p->slot_bytes;
   if (p->smem > smem_optin - 1024) return false;
   cudaFuncAttributes fa{};
@@ -1007,7 +1171,7 @@ bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p,
   p->occ = occ;
   p->sms = num_sms;
   p->nbands = (int)((g.Ho + rows - 1) / rows);
-  p->cpg = warps * ppw;
+  p->cpg = warps * (ppw == 1 ? 1 : 2);
   p->groups = (int)((g.C + p->cpg - 1) / p->cpg);
   // slices: about one wave, <= 64 tasks (image x band) per warp, <= 128 slices
   int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
