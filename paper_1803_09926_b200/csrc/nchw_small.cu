@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
   const int nwarps = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
-  const int pl = lane / 7, cg = lane - pl * 7;
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;  // lanes 28-31 shadow lane 27
   const bool live = lane < 28;
   const int c0 = cg * V;
   const T* __restrict__ in = static_cast<const T*>(a.in);
@@ -475,14 +475,18 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
   for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
   if (a.early_pdl) griddep_launch_dependents();
   const bool lft = c0 > 0, rgt = c0 + V < W;
+  // the halo columns come from the neighbouring lanes of the same plane (warp
+  // shuffles instead of two more shared-memory loads per plane and row)
   auto ldrow = [&](const T* ra, const T* rb, float2* xv) {  // .x plane A, .y plane B
     float va[V], vb[V];
     VecIO<T, V>::load(ra + c0, va);
     VecIO<T, V>::load(rb + c0, vb);
 #pragma unroll
     for (int u = 0; u < V; ++u) xv[1 + u] = make_float2(va[u], vb[u]);
-    xv[0] = lft ? make_float2(Elem<T>::load(ra + c0 - 1), Elem<T>::load(rb + c0 - 1)) : make_float2(0.f, 0.f);
-    xv[V + 1] = rgt ? make_float2(Elem<T>::load(ra + c0 + V), Elem<T>::load(rb + c0 + V)) : make_float2(0.f, 0.f);
+    const float la = __shfl_up_sync(0xffffffffu, va[V - 1], 1), lb = __shfl_up_sync(0xffffffffu, vb[V - 1], 1);
+    const float ra2 = __shfl_down_sync(0xffffffffu, va[0], 1), rb2 = __shfl_down_sync(0xffffffffu, vb[0], 1);
+    xv[0] = lft ? make_float2(la, lb) : make_float2(0.f, 0.f);
+    xv[V + 1] = rgt ? make_float2(ra2, rb2) : make_float2(0.f, 0.f);
   };
   int s = 0;
   uint32_t ph = 0;
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
       w2[k] = make_float2(Elem<T>::ldg(wt + (int64_t)ca * 9 + kk), Elem<T>::ldg(wt + (int64_t)cb2 * 9 + kk));
     }
     mbar_wait(&bars[s], ph);
-    if (live) {
+    {  // every lane runs the loop (shuffles); lanes 28-31 recompute lane 27's columns and store nothing
       const T* pa = slot(s) + pl * HW;
       const T* pb = pa + 4 * HW;
       float2 xw[3][V + 2];
@@ -520,8 +524,10 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
           oa[u] = acc.x;
           ob[u] = acc.y;
         }
-        VecIO<T, V>::store(poa + r * W, oa);
-        VecIO<T, V>::store(pob + r * W, ob);
+        if (live) {
+          VecIO<T, V>::store(poa + r * W, oa);
+          VecIO<T, V>::store(pob + r * W, ob);
+        }
 #pragma unroll
         for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
       }
