@@ -58,6 +58,19 @@ __device__ __forceinline__ void load_row(const T* row, int c0, bool lft, bool rg
   xv[V + 1] = rgt ? Elem<T>::load(row + c0 + V) : 0.f;
 }
 
+// the same row with the halo columns taken from the neighbouring lanes (warp
+// shuffles; every lane of the warp must call it)
+template <class T, int W, int V>
+__device__ __forceinline__ void load_row_shfl(const T* row, int c0, bool lft, bool rgt, float* xv) {
+  float v[V];
+  VecIO<T, V>::load(row + c0, v);
+#pragma unroll
+  for (int u = 0; u < V; ++u) xv[1 + u] = v[u];
+  const float l = __shfl_up_sync(0xffffffffu, v[V - 1], 1), r = __shfl_down_sync(0xffffffffu, v[0], 1);
+  xv[0] = lft ? l : 0.f;
+  xv[V + 1] = rgt ? r : 0.f;
+}
+
 // MODE 0 fwd, 1 bwd_data (rotated kernel)
 template <class T, int W, int MODE>
 __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
@@ -67,8 +80,8 @@ __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
   const int nwarps = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
-  const int pl = lane / 7, cg = lane - pl * 7;  // plane within the task, column group
-  const bool live = lane < 28;
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;  // plane, column group
+  const bool live = lane < 28;  // lanes 28-31 shadow lane 27 (shuffle partners only)
   const int c0 = cg * V;
   const T* __restrict__ in = static_cast<const T*>(a.in);
   T* __restrict__ out = static_cast<T*>(a.out);
@@ -100,17 +113,17 @@ __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) wr[k] = Elem<T>::ldg(wt + (int64_t)c * 9 + (MODE == 1 ? 8 - k : k));
     mbar_wait(&bars[s], ph);
-    if (live) {
+    {
       const T* pln = slot(s) + pl * HW;
       const bool lft = c0 > 0, rgt = c0 + V < W;
       float xw[3][V + 2];
 #pragma unroll
       for (int u = 0; u < V + 2; ++u) xw[0][u] = 0.f;  // row -1
-      load_row<T, W, V>(pln, c0, lft, rgt, xw[1]);
+      load_row_shfl<T, W, V>(pln, c0, lft, rgt, xw[1]);
       T* po = out + q * HW + c0;
 #pragma unroll
       for (int r = 0; r < W; ++r) {
-        if (r + 1 < W) load_row<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
+        if (r + 1 < W) load_row_shfl<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
         else
 #pragma unroll
           for (int u = 0; u < V + 2; ++u) xw[2][u] = 0.f;  // row W
@@ -122,7 +135,7 @@ __global__ void __launch_bounds__(256) small_fd_kernel(const SArgs a) {
           for (int k = 1; k < 9; ++k) acc = fmaf(wr[k], xw[k / 3][u + k % 3], acc);
           o[u] = acc;
         }
-        VecIO<T, V>::store(po + r * W, o);
+        if (live) VecIO<T, V>::store(po + r * W, o);
 #pragma unroll
         for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
       }
@@ -145,8 +158,8 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
   const int nwarps = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
-  const int pl = lane / 7, cg = lane - pl * 7;
-  const bool live = lane < 28;
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;
+  const bool live = lane < 28;  // lanes 28-31 shadow lane 27 (shuffle partners only)
   const int c0 = cg * V;
   const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
   const int cb = g * 4;  // first channel of the group
@@ -185,31 +198,31 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
   uint32_t ph = 0;
   for (int n = n0 + warp; n < n1; n += nwarps) {
     mbar_wait(&bars[s], ph);
-    if (live) {
+    {
       const T* pln = slot(s) + pl * HW;
       const T* pd = slot(s) + 4 * HW + pl * HW;
       const bool lft = c0 > 0, rgt = c0 + V < W;
       float xw[3][V + 2];
 #pragma unroll
       for (int u = 0; u < V + 2; ++u) xw[0][u] = 0.f;
-      load_row<T, W, V>(pln, c0, lft, rgt, xw[1]);
+      load_row_shfl<T, W, V>(pln, c0, lft, rgt, xw[1]);
       float loc[9];
       float dw3[FUSED ? 3 : 1][V + 2];  // dy window (fused dx)
       T* po = dxo + ((int64_t)n * a.C + cb + pl) * HW + c0;
       if constexpr (FUSED) {
 #pragma unroll
         for (int u = 0; u < V + 2; ++u) dw3[0][u] = 0.f;
-        load_row<T, W, V>(pd, c0, lft, rgt, dw3[1]);
+        load_row_shfl<T, W, V>(pd, c0, lft, rgt, dw3[1]);
       }
 #pragma unroll
       for (int r = 0; r < W; ++r) {
-        if (r + 1 < W) load_row<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
+        if (r + 1 < W) load_row_shfl<T, W, V>(pln + (r + 1) * W, c0, lft, rgt, xw[2]);
         else
 #pragma unroll
           for (int u = 0; u < V + 2; ++u) xw[2][u] = 0.f;
         float d[V];
         if constexpr (FUSED) {
-          if (r + 1 < W) load_row<T, W, V>(pd + (r + 1) * W, c0, lft, rgt, dw3[2]);
+          if (r + 1 < W) load_row_shfl<T, W, V>(pd + (r + 1) * W, c0, lft, rgt, dw3[2]);
           else
 #pragma unroll
             for (int u = 0; u < V + 2; ++u) dw3[2][u] = 0.f;
@@ -222,7 +235,7 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
             for (int k = 1; k < 9; ++k) acc = fmaf(wf[k], dw3[k / 3][u + k % 3], acc);
             o[u] = acc;
           }
-          VecIO<T, V>::store(po + r * W, o);
+          if (live) VecIO<T, V>::store(po + r * W, o);
 #pragma unroll
           for (int u = 0; u < V + 2; ++u) { dw3[0][u] = dw3[1][u]; dw3[1][u] = dw3[2][u]; }
         } else {
@@ -236,8 +249,10 @@ __global__ void __launch_bounds__(256) small_bf_kernel(const SArgs a) {
 #pragma unroll
         for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
       }
+      if (live) {
 #pragma unroll
-      for (int k = 0; k < 9; ++k) run[k] += loc[k];
+        for (int k = 0; k < 9; ++k) run[k] += loc[k];
+      }
     }
     __syncwarp();
     issue(n + a.ns * nwarps, s);
@@ -553,7 +568,7 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
   const int nwarps = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
-  const int pl = lane / 7, cg = lane - pl * 7;
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;  // lanes 28-31 shadow lane 27
   const bool live = lane < 28;
   const int c0 = cg * V;
   const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
@@ -580,14 +595,16 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
   for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
   if (a.early_pdl) griddep_launch_dependents();
   const bool lft = c0 > 0, rgt = c0 + V < W;
-  auto ldrow = [&](const T* ra, const T* rb, float2* xv) {
+  auto ldrow = [&](const T* ra, const T* rb, float2* xv) {  // halos by warp shuffles (all lanes call this)
     float va[V], vb[V];
     VecIO<T, V>::load(ra + c0, va);
     VecIO<T, V>::load(rb + c0, vb);
 #pragma unroll
     for (int u = 0; u < V; ++u) xv[1 + u] = make_float2(va[u], vb[u]);
-    xv[0] = lft ? make_float2(Elem<T>::load(ra + c0 - 1), Elem<T>::load(rb + c0 - 1)) : make_float2(0.f, 0.f);
-    xv[V + 1] = rgt ? make_float2(Elem<T>::load(ra + c0 + V), Elem<T>::load(rb + c0 + V)) : make_float2(0.f, 0.f);
+    const float la = __shfl_up_sync(0xffffffffu, va[V - 1], 1), lb = __shfl_up_sync(0xffffffffu, vb[V - 1], 1);
+    const float ra2 = __shfl_down_sync(0xffffffffu, va[0], 1), rb2 = __shfl_down_sync(0xffffffffu, vb[0], 1);
+    xv[0] = lft ? make_float2(la, lb) : make_float2(0.f, 0.f);
+    xv[V + 1] = rgt ? make_float2(ra2, rb2) : make_float2(0.f, 0.f);
   };
   float2 run[9];
 #pragma unroll
@@ -596,7 +613,7 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
   uint32_t ph = 0;
   for (int n = n0 + warp; n < n1; n += nwarps) {
     mbar_wait(&bars[s], ph);
-    if (live) {
+    {  // every lane runs the loop (shuffles); lanes 28-31 duplicate lane 27 and are left out of the sums
       const T* pa = slot(s) + pl * HW;
       const T* pb = pa + 4 * HW;
       const T* da = slot(s) + 8 * HW + pl * HW;
@@ -626,8 +643,10 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
 #pragma unroll
         for (int u = 0; u < V + 2; ++u) { xw[0][u] = xw[1][u]; xw[1][u] = xw[2][u]; }
       }
+      if (live) {
 #pragma unroll
-      for (int k = 0; k < 9; ++k) run[k] = __fadd2_rn(run[k], loc[k]);
+        for (int k = 0; k < 9; ++k) run[k] = __fadd2_rn(run[k], loc[k]);
+      }
     }
     __syncwarp();
     issue(n + a.ns * nwarps, s);
