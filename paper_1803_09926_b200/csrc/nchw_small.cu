@@ -449,7 +449,9 @@ __device__ __forceinline__ void load_row2(const T* row, int c0, float* xv) {  //
   VecIO<T, 2 * V>::load(row + 2 * c0, v);
 #pragma unroll
   for (int u = 0; u < 2 * V; ++u) xv[1 + u] = v[u];
-  xv[0] = (c0 > 0) ? Elem<T>::load(row + 2 * c0 - 1) : 0.f;
+  // the left halo is the previous lane's last column (every lane of the warp calls this)
+  const float l = __shfl_up_sync(0xffffffffu, v[2 * V - 1], 1);
+  xv[0] = (c0 > 0) ? l : 0.f;
 }
 
 // bf16 plane pairs (stride 1): a warp task is 8 planes; lane (p, column group)
@@ -693,7 +695,7 @@ __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
   const int nwarps = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
-  const int pl = lane / 7, cg = lane - pl * 7;
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;  // lanes 28-31 shadow lane 27
   const bool live = lane < 28;
   const int c0 = cg * V;
   const T* __restrict__ in = static_cast<const T*>(a.in);
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) wr[k] = Elem<T>::ldg(wt + (int64_t)c * 9 + k);
     mbar_wait(&bars[s], ph);
-    if (live) {
+    {  // every lane runs the loop (halo shuffles); only live lanes store / accumulate
       const T* pln = slot(s) + pl * HW;
       float xw[3][NXW];
 #pragma unroll
@@ -747,7 +749,7 @@ __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
           for (int k = 1; k < 9; ++k) acc = fmaf(wr[k], xw[k / 3][2 * u + k % 3], acc);
           o[u] = acc;
         }
-        VecIO<T, V>::store(po + r * Wo, o);
+        if (live) VecIO<T, V>::store(po + r * Wo, o);
 #pragma unroll
         for (int u = 0; u < NXW; ++u) xw[0][u] = xw[2][u];
       }
@@ -768,7 +770,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   const int nwarps = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
   T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
-  const int pl = lane / 7, cg = lane - pl * 7;
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;  // lanes 28-31 shadow lane 27
   const bool live = lane < 28;
   const int c0 = cg * V;
   const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
@@ -800,7 +802,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   uint32_t ph = 0;
   for (int n = n0 + warp; n < n1; n += nwarps) {
     mbar_wait(&bars[s], ph);
-    if (live) {
+    {  // every lane runs the loop (halo shuffles); only live lanes store / accumulate
       const T* pln = slot(s) + pl * HW;
       const T* pd = slot(s) + 4 * HW + pl * HWo;
       float xw[3][NXW];
@@ -825,8 +827,10 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
 #pragma unroll
         for (int u = 0; u < NXW; ++u) xw[0][u] = xw[2][u];
       }
+      if (live) {
 #pragma unroll
-      for (int k = 0; k < 9; ++k) run[k] += loc[k];
+        for (int k = 0; k < 9; ++k) run[k] += loc[k];
+      }
     }
     __syncwarp();
     issue(n + a.ns * nwarps, s);
