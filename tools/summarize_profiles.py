@@ -83,9 +83,11 @@ def main():
 
     def kind(name):
         import re as _re
-        m = _re.search(r"small_fd_kernel<[^>]*,\s*(\d)>", name)
+        m = _re.search(r"small_fd(?:_pair)?_kernel<[^>]*,\s*(\d)>", name)
         if m:  # small-plane kernel: MODE 0 = fwd, 1 = bwd_data
             return "fwd" if m.group(1) == "0" else "bwd_data"
+        if "small_fwd2_kernel" in name:
+            return "fwd"
         if "fwd_kernel" in name or "generic_fwd" in name:
             return "fwd"
         if "bwd_data" in name:
