@@ -190,7 +190,7 @@ DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* inf
  *     Returns DWCONV_ERR_BAD_DESCRIPTOR if the list was not queried first or the
  *     index is out of range.  Both are host-only calls (no launches) and
  *     thread-safe; neither may be called during stream capture of the same pass. */
-#define DWCONV_MAX_CANDIDATES 24
+#define DWCONV_MAX_CANDIDATES 32
 DWCONV_API int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, dwconv_plan_info* infos,
                                       int* count);
 DWCONV_API int dwconv_plan_select(const dwconv_desc* d, int pass, int index);

@@ -20,7 +20,7 @@ FUNCTIONS = ("dwconv_abi_version", "dwconv_status_string", "dwconv_output_shape"
              "dwconv_bwd_workspace_bytes", "dwconv_bwd",
              "dwconv_workspace_init", "dwconv_plan", "dwconv_plan_candidates", "dwconv_plan_select",
              "dwconv_set_variant_override")
-MAX_CANDIDATES = 24
+MAX_CANDIDATES = 32
 
 
 class Desc(ctypes.Structure):

@@ -488,7 +488,8 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
       // {warps, ring slots, band rows, planes per warp}
       static const int bshapes[][4] = {{4, 2, 7, 1}, {4, 3, 7, 1}, {8, 2, 7, 1}, {2, 3, 7, 1}, {4, 2, 14, 1},
                                        {8, 2, 14, 1}, {4, 2, 7, 2}, {4, 3, 7, 2}, {8, 2, 7, 2}, {4, 2, 14, 2},
-                                       {4, 2, 7, 3}, {4, 3, 7, 3}, {8, 2, 7, 3}, {4, 2, 14, 3}};
+                                       {4, 2, 7, 3}, {4, 3, 7, 3}, {8, 2, 7, 3}, {4, 2, 14, 3},
+                                       {4, 4, 7, 1}, {2, 4, 7, 1}, {4, 4, 7, 2}, {2, 4, 14, 2}};
       for (const auto& sh : bshapes) {
         ChunkPlan v;
         if (dwk::band_chunk_plan(g, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2], sh[3])) cands.push_back(v);
