@@ -149,7 +149,7 @@ struct NhwcTmaPlan {
 };
 // tw_max / stages: tile-column cap and ring depth (0 = the defaults, env DWCONV_NHWC_TW / _STAGES)
 bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* plan, int tw_max = 0,
-                   int stages = 0);
+                   int stages = 0, int th = 0);
 cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in, const void* w, void* out,
                             cudaStream_t st);
 bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* plan, int tw_max = 0,

@@ -442,6 +442,8 @@ TKernelFn pick_th(int TH) {
   if constexpr (MODE == kBd2) {
     return TH == 14 ? nhwc_tma_kernel<T, MODE, 14> : (TH == 8 ? nhwc_tma_kernel<T, MODE, 8> : nullptr);
   } else {
+    if constexpr (MODE == kFwd1 || MODE == kBd1)  // stride 1 also has two-strip (14-row) tiles
+      if (TH == 14) return nhwc_tma_kernel<T, MODE, 14>;
     return TH == 7 ? nhwc_tma_kernel<T, MODE, 7> : (TH == 8 ? nhwc_tma_kernel<T, MODE, 8> : nullptr);
   }
 }
@@ -502,7 +504,8 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 }  // namespace nhwct
 
 // Plan: mode, channel block, tile, box, ring depth, grid.  false = not eligible.
-bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* p, int tw_max, int stages) {
+bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTmaPlan* p, int tw_max, int stages,
+                   int th) {
   using namespace nhwct;
   static const int on = env_int("DWCONV_NHWC_TMA", 1, 0, 1);
   if (!on || g.layout != DWCONV_NHWC || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
@@ -526,6 +529,10 @@ bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTma
   // divisor of the output width <= the CTA's thread budget)
   int TH = (OH % 7 == 0) ? 7 : 8;
   if (p->mode == kBd2) TH = (OH % 14 == 0) ? 14 : 8;
+  if (th == 14 && (p->mode == kFwd1 || p->mode == kBd1)) {
+    if (OH % 14 != 0) return false;
+    TH = 14;
+  }
   static const int tw_max_env0 = env_int("DWCONV_NHWC_TW", 16, 1, 64);
   const int tw_max_env = tw_max > 0 ? tw_max : tw_max_env0;
   const int per_col = (p->mode == kBd2) ? 2 : 1;  // dx columns per consumer thread
