@@ -412,16 +412,15 @@ static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* 
 // NHWC candidates: the TMA family at several tile widths / ring depths, then the
 // L1 register-tile kernels.
 static void nhwc_candidates(const Geom& g, int pass, const DevInfo& di, std::vector<Plan>* cands) {
-  // {tile-column cap, ring depth, tile rows (0 = 7/8; 14 = two strips, stride-1 fwd/bwd_data)}
+  // {tile-column cap, ring depth, tile rows (0 = 7/8; 14 = two 7-row strips, stride 1)}
   static const int shapes[][3] = {{16, 2, 0}, {16, 3, 0}, {16, 4, 0}, {8, 2, 0}, {8, 3, 0}, {8, 4, 0},
                                   {4, 3, 0},  {4, 4, 0},  {32, 2, 0}, {16, 2, 14}, {16, 3, 14}, {8, 3, 14},
                                   {8, 4, 14}};
   for (const auto& sh : shapes) {
-    if (sh[2] && pass == DWCONV_PASS_BWD_FILTER) continue;
     Plan v;
     v.variant = DWCONV_VARIANT_NHWC_TMA;
     const bool ok = (pass == DWCONV_PASS_BWD_FILTER)
-                        ? dwk::plan_nhwc_tma_bf(g, di.sms, di.smem_optin, &v.tma, sh[0], sh[1])
+                        ? dwk::plan_nhwc_tma_bf(g, di.sms, di.smem_optin, &v.tma, sh[0], sh[1], sh[2])
                         : dwk::plan_nhwc_tma(g, pass, di.sms, di.smem_optin, &v.tma, sh[0], sh[1], sh[2]);
     if (!ok) continue;
     if (!dwk::plan_nhwc(g, pass, di.sms, &v.nhwc)) v.nhwc = NhwcPlan{};

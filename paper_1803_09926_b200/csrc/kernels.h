@@ -153,7 +153,7 @@ bool plan_nhwc_tma(const Geom& g, int pass, int num_sms, int smem_optin, NhwcTma
 cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in, const void* w, void* out,
                             cudaStream_t st);
 bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* plan, int tw_max = 0,
-                      int stages = 0);
+                      int stages = 0, int th = 0);
 cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* x, const void* dy, float* dw,
                                void* ws, cudaStream_t st);
 

@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(kMaxConsumers + 32) nhwc_tma_bf_kernel(const _
 
 using BKernelFn = void (*)(const CUtensorMap, const CUtensorMap, const BArgs);
 BKernelFn bf_kernel_for(int dtype, int S, int TH) {
+  if (S == 1 && TH == 14)  // two-strip tiles (stride 1)
+    return dtype == DWCONV_F32 ? nhwc_tma_bf_kernel<float, 1, 14> : nhwc_tma_bf_kernel<__nv_bfloat16, 1, 14>;
   if (dtype == DWCONV_F32) {
     if (S == 1) return TH == 7 ? nhwc_tma_bf_kernel<float, 1, 7> : nhwc_tma_bf_kernel<float, 1, 8>;
     return TH == 7 ? nhwc_tma_bf_kernel<float, 2, 7> : nhwc_tma_bf_kernel<float, 2, 8>;
@@ -630,7 +632,8 @@ cudaError_t launch_nhwc_tma(const Geom& g, const NhwcTmaPlan& p, const void* in,
   return cudaLaunchKernelEx(&cfg, fn, tm, a);
 }
 
-bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p, int tw_max, int stages) {
+bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p, int tw_max, int stages,
+                      int th) {
   using namespace nhwct;
   static const int on = env_int("DWCONV_NHWC_TMA", 1, 0, 1);
   if (!on || g.layout != DWCONV_NHWC || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
@@ -646,7 +649,11 @@ bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p
   while (CB > VC && (g.C % CB != 0 || CB % VC != 0)) CB -= VC;
   if (g.C % CB != 0 || (CB * eb) % 16 != 0) return false;
   const int NCV = (int)(CB / VC);
-  const int TH = (g.Ho % 7 == 0) ? 7 : 8;
+  int TH = (g.Ho % 7 == 0) ? 7 : 8;
+  if (th == 14) {
+    if (S != 1 || g.Ho % 14 != 0) return false;
+    TH = 14;
+  }
   static const int tw_env0 = env_int("DWCONV_NHWC_TW", 16, 1, 64);
   const int tw_env = tw_max > 0 ? tw_max : tw_env0;
   const int tw_cap = std::max(1, std::min(tw_env, kMaxConsumers / NCV));
