@@ -9,6 +9,8 @@ follows), and this module only marshals numpy arrays into it.
 
 Parity status of each function (DESIGN.md §4 lists the pins):
   fwd, bwd_data, bwd_filter    pinned: P1-P8 in tests/test_oracle.py
+  their sum|terms| outputs     pinned: P7b (torch CPU fp64 conv2d / conv2d_input /
+                               conv2d_weight of |x|, |w|, |dy|: bitwise on integers)
   dense_* / expand / mask      pinned: P7 (torch CPU fp64 conv2d), P1/P2
   round (storage rounding)     pinned: numpy fp32 casts, hand-built bf16 cases
 """

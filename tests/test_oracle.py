@@ -256,6 +256,47 @@ def test_p7_property_random_specs(N, C, H, W, m, K, s, p, layout):
     _check_torch((N, C, H, W, m, K, s, p), _ints, layout)
 
 
+# ---------------------------------------------------------------- P7b: the tolerance basis
+# Every float parity tolerance (R11/R13) is scaled by the oracle's per-element
+# sum|terms|.  The terms are products of two inputs, so sum|terms| is the same
+# convolution applied to |x|, |w| (fwd), |dy|, |w| (bwd_data), |x|, |dy|
+# (bwd_filter) over the same in-bounds taps: torch's fp64 conv2d of the absolute
+# values computes it independently.  An inflated (out-of-range taps, wrong j
+# loop) or deflated sum fails here; on integers the match is bitwise.
+def _check_abs_sums(spec, gen, layout):
+    N, C, H, W, m, K, s, p = spec
+    x, w, dy = _data(spec, gen)
+    ty, tdx, tdw = _torch_ref(np.abs(x), np.abs(w), np.abs(dy), C, s, p)
+    xl, dyl = _to_layout(x, layout), _to_layout(dy, layout)
+    ay = _from_layout(oracle.fwd(xl, w, s, p, layout)[1], layout)
+    adx = _from_layout(oracle.bwd_data(dyl, w, xl.shape, s, p, layout)[1], layout)
+    adw = oracle.bwd_filter(xl, dyl, w.shape, s, p, layout)[1]
+    for name, a, t in (("ABS_y", ay, ty), ("ABS_dx", adx, tdx), ("ABS_dw", adw, tdw)):
+        if gen is _ints:
+            assert np.array_equal(a, t), name
+        else:
+            assert np.all(np.abs(a - t) <= 1e-13 * t + 1e-300), (name, np.max(np.abs(a - t) / (t + 1e-300)))
+
+
+@pytest.mark.parametrize("layout", [NCHW, NHWC])
+@pytest.mark.parametrize("spec", SPECS)
+def test_p7b_abs_sums_equal_conv_of_abs_values(spec, layout):
+    _check_abs_sums(spec, _ints, layout)
+    _check_abs_sums(spec, _unif, layout)
+
+
+@settings(max_examples=40, deadline=None)
+@given(N=st.integers(1, 2), C=st.integers(1, 5), H=st.integers(1, 9), W=st.integers(1, 9),
+       m=st.integers(1, 3), K=st.sampled_from([1, 2, 3, 5, 7]), s=st.integers(1, 3),
+       p=st.integers(0, 4), layout=st.sampled_from([NCHW, NHWC]))
+def test_p7b_abs_sums_property(N, C, H, W, m, K, s, p, layout):
+    p = min(p, K - 1)
+    if H + 2 * p < K or W + 2 * p < K:
+        return
+    _check_abs_sums((N, C, H, W, m, K, s, p), _ints, layout)
+    _check_abs_sums((N, C, H, W, m, K, s, p), _unif, layout)
+
+
 def test_rectangular_kernel_stride_pad_against_torch():
     x, w = _ints(1, (2, 3, 9, 11)), _ints(2, (6, 3, 5))
     y, _ = oracle.fwd(x, w, (2, 1), (1, 2))

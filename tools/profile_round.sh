@@ -14,6 +14,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 for spec in ${2:-}; do
   set -- ${spec//:/ }
   ncu --set full --clock-control none --import-source on -k regex:"nchw|dbf|nhwc|small_|band_" -s 1 -c 1 -o /tmp/prof/full_$1_$2 \
-      python tools/run_layer.py --layer $1 --pass $2 --reps 2 --plans /tmp/prof/plans.json > /dev/null 2>&1
+      python tools/run_layer.py --layer $1 --pass $2 --reps 2 --plans /tmp/prof/plans.json $args > /dev/null 2>&1
   ncu -i /tmp/prof/full_$1_$2.ncu-rep --page raw --csv > $out/raw_$1_$2.csv 2>&1
 done

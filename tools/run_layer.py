@@ -21,7 +21,7 @@ ap.add_argument("--layout", default="nchw")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--plan", action="store_true")
 ap.add_argument("--plans", default="", help="bench.py --plans file: install this layer's measured selection")
-a = ap.parse_args()
+a, _unknown = ap.parse_known_args()  # bench.py args pass through (profile_round.sh)
 L = [l for l in synth.mobilenet_v1_dw(a.batch, a.alpha, a.res) if l.name == a.layer][0]
 lay = dwl.NCHW if a.layout == "nchw" else dwl.NHWC
 dt = torch.float32 if a.dtype == "f32" else torch.bfloat16
