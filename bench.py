@@ -10,8 +10,12 @@ bucket (44,640 fp32).  Default workload: BASELINE.json configs[1] -- width 1.0,
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
+    torchrun --nproc-per-node N bench.py --gpus N --global-batch 1024   # configs[4], strong scaling
 
-Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every field).
+Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every field).  At N=1 the
+line also carries ``workloads_b128``: the north star's >= 70 % target set
+(alpha 1.0 / 224 at batch 128: fp32 NCHW, bf16 NCHW, bf16 NHWC), each measured
+the same way in the same process.
 """
 from __future__ import annotations
 
@@ -30,16 +34,21 @@ import numpy as np  # noqa: E402
 
 METRIC = "MobileNet-v1 depthwise fwd+bwd images/s and achieved HBM GB/s (% peak), 1/2/4/8 B200"
 FALLBACK_HBM_GBS = 6650.0
+NOMINAL_HBM_GBS = 8000.0          # BASELINE north star "~8 TB/s peak"; the >= 70 % target is stated on it
+NVLINK_GBS_PER_DIR = 900.0        # NVLink 5, per GPU per direction (the all-reduce roofline basis)
 PAPER_CONTEXT_IMG_S = 445.0  # Table III Diagonalwise cuDNN fwd+bwd, x5-corrected, GTX 1080 Ti
+B128_SET = (("f32", "nchw"), ("bf16", "nchw"), ("bf16", "nhwc"))
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=64, help="images per GPU")
+    ap.add_argument("--batch", type=int, default=64, help="images per GPU (weak scaling)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="total images split over the ranks with dp.shard_batch (configs[4]: 1024; strong scaling)")
     ap.add_argument("--alpha", type=float, default=1.0)
     ap.add_argument("--res", type=int, default=224)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
@@ -52,21 +61,22 @@ def parse():
     ap.add_argument("--no-tune", action="store_true", help="keep the planner's launch shapes (no measured selection)")
     ap.add_argument("--plans", default="", help="JSON file of measured plan selections: loaded if it exists, else written")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget (cpu_baseline)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="oracle sample budget per cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--kernel-reps", type=int, default=5, help="graph replays per kernel in the per-kernel timing")
+    ap.add_argument("--no-b128", action="store_true", help="skip the batch-128 target-set workloads (N=1 only)")
+    ap.add_argument("--b128-steps", type=int, default=50)
     ap.add_argument("--extra", action="store_true", help="add per-layer kernel table to the JSON line")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
-def layers_for(args, batch):
+def layers_for(alpha, res, batch):
     import synth
-    return synth.mobilenet_v1_dw(batch, alpha=args.alpha, resolution=args.res)
+    return synth.mobilenet_v1_dw(batch, alpha=alpha, resolution=res)
 
 
-def workload_name(args):
-    w = f"mobilenet_v1_a{args.alpha:g}_r{args.res}_dw13"
-    return w
+def workload_name(alpha, res):
+    return f"mobilenet_v1_a{alpha:g}_r{res}_dw13"
 
 
 def step_bytes(layers, eb, fused=None):
@@ -80,13 +90,17 @@ def step_bytes(layers, eb, fused=None):
 
 
 def pass_bytes(L, pas, eb):
-    if pas == "fwd":
-        return (L.x_elems() + L.y_elems() + L.w_elems()) * eb
-    if pas == "bwd_data":
+    if pas in ("fwd", "bwd_data"):
         return (L.x_elems() + L.y_elems() + L.w_elems()) * eb
     if pas == "bwd":  # fused: x, dy, w read; dx, dw written
         return (2 * L.x_elems() + L.y_elems() + L.w_elems()) * eb + L.w_elems() * 4
     return (L.x_elems() + L.y_elems()) * eb + L.w_elems() * 4
+
+
+def dev_env():
+    """DWCONV_* variables in the environment.  The shipped library reads none of them (launch-shape knobs
+    exist only in a -DDWCONV_DEV_KNOBS build), so they cannot change a timed launch; recorded anyway."""
+    return {k: v for k, v in os.environ.items() if k.startswith("DWCONV_")}
 
 
 # ------------------------------------------------------------------ clocks
@@ -149,34 +163,74 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ oracle timing (CPU)
-def oracle_sample(layers, s_budget, max_images=64):
+def oracle_sample(layers, s_budget, max_images=64, threads=1):
     """Time the oracle on images of the workload until ~s_budget seconds; returns (img/s, images, secs)."""
     import oracle
     import synth
     oracle.build()
-    t0 = time.perf_counter()
-    done = 0
-    while done < max_images:
-        for li, L in enumerate(layers):
-            x = synth.uniform(synth.layer_seed(li, "x"), (1, L.c, L.h, L.w), start=done * L.c * L.h * L.w)
-            w = synth.uniform(synth.layer_seed(li, "w"), (L.c * L.m, L.k, L.k))
-            dy = synth.uniform(synth.layer_seed(li, "dy"), (1, L.c * L.m, L.ho, L.wo),
-                               start=done * L.c * L.m * L.ho * L.wo)
-            oracle.fwd(x, w, L.s, L.p)
-            oracle.bwd_data(dy, w, x.shape, L.s, L.p)
-            oracle.bwd_filter(x, dy, w.shape, L.s, L.p)
-        done += 1
-        if time.perf_counter() - t0 >= s_budget:
-            break
-    secs = time.perf_counter() - t0
+    oracle.set_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        done = 0
+        while done < max_images:
+            for li, L in enumerate(layers):
+                x = synth.uniform(synth.layer_seed(li, "x"), (1, L.c, L.h, L.w), start=done * L.c * L.h * L.w)
+                w = synth.uniform(synth.layer_seed(li, "w"), (L.c * L.m, L.k, L.k))
+                dy = synth.uniform(synth.layer_seed(li, "dy"), (1, L.c * L.m, L.ho, L.wo),
+                                   start=done * L.c * L.m * L.ho * L.wo)
+                oracle.fwd(x, w, L.s, L.p)
+                oracle.bwd_data(dy, w, x.shape, L.s, L.p)
+                oracle.bwd_filter(x, dy, w.shape, L.s, L.p)
+            done += 1
+            if time.perf_counter() - t0 >= s_budget:
+                break
+        secs = time.perf_counter() - t0
+    finally:
+        oracle.set_threads(1)
     return done / secs, done, secs
+
+
+def oracle_threads_bitwise(layers, threads):
+    """The all-cores oracle must give bitwise the single-thread results: checked on one
+    image of the last layer (all three passes) before its time is reported."""
+    import oracle
+    import synth
+    li = len(layers) - 1
+    L = layers[li]
+    x = synth.uniform(synth.layer_seed(li, "x"), (2, L.c, L.h, L.w))
+    w = synth.uniform(synth.layer_seed(li, "w"), (L.c * L.m, L.k, L.k))
+    dy = synth.uniform(synth.layer_seed(li, "dy"), (2, L.c * L.m, L.ho, L.wo))
+    outs = []
+    for t in (1, threads):
+        oracle.set_threads(t)
+        outs.append([oracle.fwd(x, w, L.s, L.p), oracle.bwd_data(dy, w, x.shape, L.s, L.p),
+                     oracle.bwd_filter(x, dy, w.shape, L.s, L.p)])
+    oracle.set_threads(1)
+    return all(np.array_equal(a, b) for r1, r2 in zip(*outs) for a, b in zip(r1, r2))
+
+
+def cpu_baselines(layers, s_budget):
+    cores = len(os.sched_getaffinity(0))
+    v1, n1, s1 = oracle_sample(layers, s_budget, threads=1)
+    single = {"value": v1, "unit": "images/s", "cores": 1, "kind": "oracle",
+              "sample": f"{n1} images of the 13-layer stack (fwd+bwd_data+bwd_filter), plain-C fp64 oracle, "
+                        f"single thread, {s1:.1f} s"}
+    allc = None
+    if cores > 1:
+        same = oracle_threads_bitwise(layers, cores)
+        va, na, sa = oracle_sample(layers, s_budget, max_images=256, threads=cores)
+        allc = {"value": va, "unit": "images/s", "cores": cores, "kind": "oracle",
+                "bitwise_equal_to_single_thread": same,
+                "sample": f"{na} images of the 13-layer stack, same oracle with its outer loops over {cores} "
+                          f"OpenMP threads, {sa:.1f} s"}
+    return single, allc
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    layers = layers_for(args, 1)
+    layers = layers_for(args.alpha, args.res, 1)
     import oracle
     oracle.build()
     times = []
@@ -193,8 +247,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 U[-1,1])",
-        "config": {"workload": workload_name(args), "batch_per_gpu": args.batch, "dtype_storage": args.dtype,
-                   "layout": args.layout, "sample": "1 image per step"},
+        "config": {"workload": workload_name(args.alpha, args.res), "batch_per_gpu": args.batch,
+                   "dtype_storage": args.dtype, "layout": args.layout, "sample": "1 image per step"},
         "hbm_gbs": None,
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": 1, "kind": "oracle",
                          "sample": "each step = 1 image of the 13-layer stack, fwd+bwd_data+bwd_filter, "
@@ -207,14 +261,259 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
-def main():
-    args = parse()
+def hbm_peak():
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def pct(v, q):
+    return float(np.percentile(np.asarray(v, dtype=np.float64), q))
+
+
+class Workload:
+    """Every buffer of one bench workload: NSETS complete input/output sets (x, dy, y, dx per layer) that
+    successive steps alternate between, shared weights and one flat dw bucket; the measured plan
+    selection; one CUDA graph per set."""
+    NSETS = 2
+
+    def __init__(self, torch, dev, rank, alpha, res, batch, dtype, layout, fused_mode="none", tune=True,
+                 plans_file="", serial=False, graph=True):
+        import paper_1803_09926_b200 as dwl
+        from paper_1803_09926_b200 import dp, ops
+        self.torch, self.ops, self.dev = torch, ops, dev
+        self.alpha, self.res, self.batch, self.dtype, self.layout = alpha, res, batch, dtype, layout
+        self.serial = serial
+        lay = dwl.NCHW if layout == "nchw" else dwl.NHWC
+        dcode = dwl.F32 if dtype == "f32" else dwl.BF16
+        tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+        self.eb = 4 if dtype == "f32" else 2
+        mf = torch.channels_last if lay == dwl.NHWC else torch.contiguous_format
+        self.layers = layers_for(alpha, res, batch)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1234 + rank)
+
+        def rnd(shape):
+            t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=gen)
+            return t.to(tdt).contiguous(memory_format=mf) if len(shape) == 4 else t.to(tdt)
+
+        self.bucket = dp.DwBucket([(L.c * L.m, L.k, L.k) for L in self.layers], device=dev)
+        self.descs, self.w, self.fused = [], [], []
+        self.sets = [[] for _ in range(self.NSETS)]
+        for li, L in enumerate(self.layers):
+            d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, lay, dcode)
+            self.descs.append(d)
+            self.w.append(rnd((L.c * L.m, L.k, L.k)))
+            for s in self.sets:
+                s.append(dict(x=rnd((L.n, L.c, L.h, L.w)), dy=rnd((L.n, L.c * L.m, L.ho, L.wo)),
+                              y=torch.empty((L.n, L.c * L.m, L.ho, L.wo), dtype=tdt, device=dev, memory_format=mf),
+                              dx=torch.empty((L.n, L.c, L.h, L.w), dtype=tdt, device=dev, memory_format=mf)))
+            self.fused.append((fused_mode == "all" or (fused_mode == "small" and L.h <= 14)) and L.n > 0 and
+                              ops.dwconv_plan(d, 3)["variant_name"] != "none")
+        # measured plan selection (tune.py): every candidate launch shape of each pass timed on this
+        # layer's tensors, the fastest kept (before any graph capture)
+        self.tuned = {}
+        if tune:
+            from paper_1803_09926_b200 import tune as tn
+            saved = None
+            if plans_file and os.path.exists(plans_file):
+                with open(plans_file) as f:
+                    saved = json.load(f)
+            for li, L in enumerate(self.layers):
+                if L.n == 0:
+                    continue
+                if saved is not None:  # re-install a saved selection (no timing: e.g. under ncu)
+                    self.tuned[L.name] = saved[L.name]
+                    tn.apply_selection(self.descs[li], self.tuned[L.name])
+                else:
+                    s0 = self.sets[0][li]
+                    self.tuned[L.name] = tn.tune_layer(self.descs[li], s0["x"], s0["dy"], self.w[li],
+                                                       passes=("fwd", "bwd") if self.fused[li] else
+                                                       ("fwd", "bwd_data", "bwd_filter"))
+            torch.cuda.synchronize()
+            if plans_file and saved is None and rank == 0:
+                with open(plans_file, "w") as f:
+                    json.dump(self.tuned, f)
+        wsb = [ops.dwconv_bwd_filter_workspace_bytes(d) for d in self.descs]
+        self.ws = torch.zeros(max([16] + wsb), dtype=torch.uint8, device=dev)
+        self.wsf = torch.zeros(max([16] + [ops.dwconv_bwd_workspace_bytes(d) for d, f in zip(self.descs, self.fused)
+                                           if f]), dtype=torch.uint8, device=dev)
+        self.footprint = sum(t.numel() * t.element_size() for s in self.sets for b in s for t in b.values())
+        self.side = torch.cuda.Stream(device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.graphs = None
+        if graph:
+            with torch.cuda.stream(self.stream):
+                for k in range(self.NSETS):
+                    for _ in range(2):
+                        self.step_kernels(k)
+                torch.cuda.synchronize()
+                self.graphs = []
+                for k in range(self.NSETS):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=self.stream):
+                        self.step_kernels(k)
+                    self.graphs.append(g)
+                torch.cuda.synchronize()
+
+    # -- launches (each one call of the C ABI through the binding)
+    def launch(self, pas, li, b):
+        ops, d = self.ops, self.descs[li]
+        if pas == "fwd":
+            ops.dwconv_fwd(d, b["x"], self.w[li], b["y"])
+        elif pas == "bwd_data":
+            ops.dwconv_bwd_data(d, b["dy"], self.w[li], b["dx"])
+        elif pas == "bwd_filter":
+            ops.dwconv_bwd_filter(d, b["x"], b["dy"], self.bucket.views[li], self.ws)
+        else:
+            ops.dwconv_bwd(d, b["x"], b["dy"], self.w[li], b["dx"], self.bucket.views[li], self.wsf)
+
+    def kernel_list(self):
+        ks = [("fwd", li) for li in range(len(self.layers))]
+        for li in reversed(range(len(self.layers))):
+            ks += [("bwd", li)] if self.fused[li] else [("bwd_data", li), ("bwd_filter", li)]
+        return [(p, li) for p, li in ks if self.layers[li].n > 0]
+
+    def step_kernels(self, k):
+        """fwd 13 layers, then per layer (reverse order) bwd_data on the main stream and bwd_filter on a
+        side stream.  bwd_filter(L) needs only x_L and dy_L, so it may run as soon as dy_L exists (here:
+        when the main stream reaches layer L's backward) and overlaps the remaining input-gradient chain
+        -- the dependency structure of a real training step (dw is off the critical path).  --serial keeps
+        every launch on one stream."""
+        torch = self.torch
+        s = self.sets[k]
+        if self.serial:
+            for pas, li in self.kernel_list():
+                self.launch(pas, li, s[li])
+            return
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        for pas, li in self.kernel_list():
+            if pas == "fwd" or pas == "bwd":
+                self.launch(pas, li, s[li])
+            elif pas == "bwd_data":
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                self.side.wait_event(ev)
+                with torch.cuda.stream(self.side):
+                    self.launch("bwd_filter", li, s[li])
+                self.launch("bwd_data", li, s[li])
+        ev = torch.cuda.Event()
+        ev.record(self.side)
+        cur.wait_event(ev)
+
+    def one_step(self, k):
+        if self.graphs is not None:
+            self.graphs[k % self.NSETS].replay()
+        else:
+            self.step_kernels(k % self.NSETS)
+
+    def timed_steps(self, steps, warmup, allreduce=None, barrier=None):
+        """K steps alternating the input sets; an event between steps gives the per-step times."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            for i in range(warmup):
+                self.one_step(i)
+                if allreduce:
+                    allreduce()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(self.stream):
+            evs[0].record(self.stream)
+            for i in range(steps):
+                self.one_step(i)
+                if allreduce:
+                    allreduce()
+                evs[i + 1].record(self.stream)
+        torch.cuda.synchronize()
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+        return evs[0].elapsed_time(evs[-1]) / steps, per
+
+    def kernel_times(self, reps):
+        """Per-kernel durations: back-to-back launches of one kernel from a CUDA graph, cycling over enough
+        copies of its tensors that their footprint is >= 2x L2 (inputs come from HBM),
+        CUDA events around the replay on the launching stream."""
+        torch = self.torch
+        l2 = torch.cuda.get_device_properties(self.dev).L2_cache_size
+        kt = []
+        for pas, li in self.kernel_list():
+            L = self.layers[li]
+            b = self.sets[0][li]
+            set_bytes = sum(b[k].numel() * b[k].element_size() for k in ("x", "dy", "y", "dx"))
+            nsets = int(max(2, min(16, -(-2 * l2 // set_bytes))))
+            sets = [b, self.sets[1][li]] + [{k: torch.empty_like(v) for k, v in b.items()}
+                                            for _ in range(max(0, nsets - 2))]
+            for bs in sets[2:]:
+                bs["x"].copy_(b["x"])
+                bs["dy"].copy_(b["dy"])
+            nsets = len(sets)
+            nl = 2 * nsets
+            with torch.cuda.stream(self.stream):
+                for bs in sets:
+                    self.launch(pas, li, bs)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    for j in range(nl):
+                        self.launch(pas, li, sets[j % nsets])
+                g.replay()
+                torch.cuda.synchronize()
+                e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e_a.record(self.stream)
+                for _ in range(reps):
+                    g.replay()
+                e_b.record(self.stream)
+            torch.cuda.synchronize()
+            mean_ms = e_a.elapsed_time(e_b) / (reps * nl)
+            del g, sets
+            nbytes = pass_bytes(L, pas, self.eb)
+            kt.append(dict(layer=L.name, pass_=pas, ms=mean_ms, bytes=nbytes, gbs=nbytes / (mean_ms * 1e-3) / 1e9,
+                           li=li))
+        return kt
+
+    def step_bytes(self):
+        return step_bytes(self.layers, self.eb, self.fused)
+
+    def plans_note(self):
+        if not self.tuned:
+            return "planner defaults"
+        ch = sum(1 for t in self.tuned.values() for v in t.values() if v["index"] != 0)
+        return (f"measured selection (tune.py, before the timed region): {ch} of "
+                f"{sum(len(t) for t in self.tuned.values())} tuned passes changed")
+
+
+def b128_workload(torch, dev, dtype, layout, steps, peak):
+    """One entry of the >= 70 %-of-HBM target set (alpha 1.0 / 224, batch 128), same harness."""
+    wl = Workload(torch, dev, 0, 1.0, 224, 128, dtype, layout)
+    ms, per = wl.timed_steps(steps, 5)
+    gbs = wl.step_bytes() / (ms / 1e3) / 1e9
+    kt = wl.kernel_times(3)
+    slow = min(kt, key=lambda k: k["gbs"] / 1.0)
+    out = {"workload": workload_name(1.0, 224), "batch": 128, "dtype": dtype, "layout": layout, "steps": steps,
+           "value": 128 / (ms / 1e3), "unit": "images/s", "ms_per_step": ms,
+           "step_ms": {"p10": pct(per, 10), "p50": pct(per, 50), "p90": pct(per, 90)},
+           "hbm_gbs": gbs, "frac_of_measured_peak": gbs / peak, "frac_of_8tbs": gbs / NOMINAL_HBM_GBS,
+           "lowest_kernel": {"kernel": f"{slow['layer']}/{slow['pass_']}", "gbs": slow["gbs"],
+                             "frac": slow["gbs"] / peak},
+           "plans": wl.plans_note()}
+    del wl
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
     import torch
     import torch.distributed as dist
-    import paper_1803_09926_b200 as dwl
-    from paper_1803_09926_b200 import dp, ops
+    from paper_1803_09926_b200 import dp
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -223,219 +522,75 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    layout = dwl.NCHW if args.layout == "nchw" else dwl.NHWC
-    dcode = dwl.F32 if args.dtype == "f32" else dwl.BF16
-    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
-    eb = 4 if args.dtype == "f32" else 2
-    mf = torch.channels_last if layout == dwl.NHWC else torch.contiguous_format
-    layers = layers_for(args, args.batch)
+    strong = args.global_batch > 0
+    if strong:
+        _, batch = dp.shard_batch(args.global_batch, world, rank)
+        total_images = args.global_batch
+    else:
+        batch = args.batch
+        total_images = args.batch * world
+    peak, peak_src = hbm_peak()
 
-    # ---- buffers: distinct per layer; weights and dw bucket shared (flat)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-
-    def rnd(shape, dtype=tdt):
-        t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=gen)
-        return t.to(dtype).contiguous(memory_format=mf) if len(shape) == 4 else t.to(dtype)
-
-    bucket = dp.DwBucket([(L.c * L.m, L.k, L.k) for L in layers], device=dev)  # every layer's dw, one all-reduce
-    dw_bucket = bucket.flat
-    bufs = []
-    for L in layers:
-        d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout, dcode)
-        b = dict(L=L, d=d, x=rnd((L.n, L.c, L.h, L.w)), w=rnd((L.c * L.m, L.k, L.k)),
-                 dy=rnd((L.n, L.c * L.m, L.ho, L.wo)),
-                 y=torch.empty((L.n, L.c * L.m, L.ho, L.wo), dtype=tdt, device=dev, memory_format=mf),
-                 dx=torch.empty((L.n, L.c, L.h, L.w), dtype=tdt, device=dev, memory_format=mf),
-                 dw=bucket.views[len(bufs)],
-                 wsb=ops.dwconv_bwd_filter_workspace_bytes(d))
-        bufs.append(b)
-    # fused backward (dx + dw in one pass over x and dy) where the library has the kernel
-    for b in bufs:
-        b["fused"] = (args.fused == "all" or (args.fused == "small" and b["L"].h <= 14)) and \
-            ops.dwconv_plan(b["d"], 3)["variant_name"] != "none"
-    # measured plan selection (tune.py): time every candidate launch shape of each
-    # pass on this layer's tensors and keep the fastest (before any graph capture)
-    tuned = {}
-    if not args.no_tune:
-        from paper_1803_09926_b200 import tune
-        saved = None
-        if args.plans and os.path.exists(args.plans):
-            with open(args.plans) as f:
-                saved = json.load(f)
-        for b in bufs:
-            if saved is not None:  # re-install a saved selection (no timing: e.g. under ncu)
-                tuned[b["L"].name] = saved[b["L"].name]
-                tune.apply_selection(b["d"], tuned[b["L"].name])
-            else:
-                tuned[b["L"].name] = tune.tune_layer(b["d"], b["x"], b["dy"], b["w"],
-                                                     passes=("fwd", "bwd") if b["fused"] else
-                                                     ("fwd", "bwd_data", "bwd_filter"))
-            b["wsb"] = ops.dwconv_bwd_filter_workspace_bytes(b["d"])
-        torch.cuda.synchronize()
-        if args.plans and saved is None and rank == 0:
-            with open(args.plans, "w") as f:
-                json.dump(tuned, f)
-    ws = torch.zeros(max(16, max(b["wsb"] for b in bufs)), dtype=torch.uint8, device=dev)
-    footprint = sum(b[k].numel() * b[k].element_size() for b in bufs for k in ("x", "w", "dy", "y", "dx"))
-
-    def launch_fwd(b):
-        ops.dwconv_fwd(b["d"], b["x"], b["w"], b["y"])
-
-    def launch_bd(b):
-        ops.dwconv_bwd_data(b["d"], b["dy"], b["w"], b["dx"])
-
-    def launch_bf(b):
-        ops.dwconv_bwd_filter(b["d"], b["x"], b["dy"], b["dw"], ws)
-
-    wsf = torch.zeros(max([16] + [ops.dwconv_bwd_workspace_bytes(b["d"]) for b in bufs if b["fused"]]),
-                      dtype=torch.uint8, device=dev)
-
-    def launch_bwd(b):
-        ops.dwconv_bwd(b["d"], b["x"], b["dy"], b["w"], b["dx"], b["dw"], wsf)
-
-    kernels = [("fwd", b, launch_fwd) for b in bufs]
-    for b in reversed(bufs):
-        kernels += [("bwd", b, launch_bwd)] if b["fused"] else [("bwd_data", b, launch_bd), ("bwd_filter", b, launch_bf)]
-
-    side = torch.cuda.Stream(device=dev)
-
-    def step_kernels():
-        """fwd 13 layers, then per layer (reverse order) bwd_data on the main stream and
-        bwd_filter on a side stream.  bwd_filter(L) needs only x_L and dy_L, so it may
-        run as soon as dy_L exists (here: when the main stream reaches layer L's
-        backward) and overlaps the remaining input-gradient chain -- the dependency
-        structure of a real training step (dw is off the critical path).  --serial
-        keeps every launch on one stream."""
-        if args.serial:
-            for _, b, f in kernels:
-                f(b)
-            return
-        cur = torch.cuda.current_stream()
-        for b in bufs:
-            launch_fwd(b)
-        for b in reversed(bufs):
-            if b["fused"]:
-                launch_bwd(b)
-                continue
-            ev = torch.cuda.Event()
-            ev.record(cur)
-            side.wait_event(ev)
-            with torch.cuda.stream(side):
-                launch_bf(b)
-            launch_bd(b)
-        ev = torch.cuda.Event()
-        ev.record(side)
-        cur.wait_event(ev)
-
-    stream = torch.cuda.Stream(device=dev)
-    graph = None
-    with torch.cuda.stream(stream):
-        for _ in range(3):
-            step_kernels()
-        torch.cuda.synchronize()
-        if not args.no_graph:
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
-                step_kernels()
-            torch.cuda.synchronize()
-
-    def one_step():
-        if graph is not None:
-            graph.replay()
-        else:
-            step_kernels()
-        if world > 1:
-            bucket.allreduce()
-
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            one_step()
-    torch.cuda.synchronize()
+    wl = Workload(torch, dev, rank, args.alpha, args.res, batch, args.dtype, args.layout, args.fused,
+                  tune=not args.no_tune, plans_file=args.plans, serial=args.serial, graph=not args.no_graph)
+    allreduce = (lambda: wl.bucket.allreduce()) if world > 1 else None
+    barrier = (lambda: dist.barrier()) if world > 1 else None
 
     # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the launching stream
     sampler = ClockSampler(local)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     sampler.start()
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(args.steps):
-            one_step()
-        e1.record(stream)
-    torch.cuda.synchronize()
+    ms_local, per = wl.timed_steps(args.steps, args.warmup, allreduce, barrier)
     sampler.stop()
     if world > 1:
         dist.barrier()
-    ms_local = e0.elapsed_time(e1) / args.steps
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    images = args.batch * world
-    value = images / (ms / 1000.0)
-    sbytes = step_bytes(layers, eb, [b["fused"] for b in bufs])
-    hbm_gbs = sbytes * world / (ms / 1000.0) / 1e9
+    value = total_images / (ms / 1000.0)
+    sbytes_local = wl.step_bytes()
+    sb = torch.tensor([float(sbytes_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(sb)
+    sbytes = int(sb.item())
+    hbm_gbs = sbytes / (ms / 1000.0) / 1e9
 
-    # ---- per-kernel durations: back-to-back launches of one kernel from a CUDA graph,
-    # cycling over enough copies of its tensors that their footprint is >= 2x L2 (inputs
-    # come from HBM, SURVEY §8(d) d.5), CUDA events around the replay on the launching stream
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    reps = args.kernel_reps  # 0: skip (e.g. under ncu, so the last launches are one step in order)
-    kt = []
-    for pas, b, f in (kernels if reps > 0 else []):
-        L = b["L"]
-        set_bytes = sum(b[k].numel() * b[k].element_size() for k in ("x", "dy", "y", "dx"))
-        nsets = int(max(2, min(16, -(-2 * l2 // set_bytes))))
-        sets = [b] + [dict(b, x=torch.empty_like(b["x"]), dy=torch.empty_like(b["dy"]), y=torch.empty_like(b["y"]),
-                           dx=torch.empty_like(b["dx"])) for _ in range(nsets - 1)]
-        for bs in sets[1:]:
-            bs["x"].copy_(b["x"]); bs["dy"].copy_(b["dy"])
-        nl = 2 * nsets
-        with torch.cuda.stream(stream):
-            for bs in sets:
-                f(bs)
+    # ---- the all-reduce alone (N > 1): its time, bus bandwidth, NVLink-roofline fraction
+    comm = None
+    if world > 1:
+        with torch.cuda.stream(wl.stream):
+            for _ in range(5):
+                wl.bucket.allreduce()
             torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for j in range(nl):
-                    f(sets[j % nsets])
-            g.replay()
-            torch.cuda.synchronize()
-            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e_a.record(stream)
-            for _ in range(reps):
-                g.replay()
-            e_b.record(stream)
+            dist.barrier()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(wl.stream)
+            for _ in range(50):
+                wl.bucket.allreduce()
+            c1.record(wl.stream)
         torch.cuda.synchronize()
-        mean_ms = e_a.elapsed_time(e_b) / (reps * nl)
-        del g, sets
-        nbytes = pass_bytes(L, pas, eb)
-        kt.append(dict(layer=L.name, pass_=pas, ms=mean_ms, bytes=nbytes, gbs=nbytes / (mean_ms * 1e-3) / 1e9))
-        if args.extra:
-            pl = ops.dwconv_plan(b["d"], {"fwd": 0, "bwd_data": 1, "bwd_filter": 2, "bwd": 3}[pas])
-            kt[-1]["plan"] = {k: pl[k] for k in ("variant_name", "grid", "block", "smem_bytes", "work_units",
-                                                 "planes_per_chunk", "rows_per_band", "batch_slices")}
+        ar_us = c0.elapsed_time(c1) * 1e3 / 50
+        t = torch.tensor([ar_us], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ar_us = float(t.item())
+        busbw = 2.0 * (world - 1) / world * wl.bucket.nbytes / (ar_us * 1e-6) / 1e9
+        comm = {"allreduce_us": ar_us, "bytes": wl.bucket.nbytes, "bus_gbs": busbw,
+                "nvlink_frac": busbw / NVLINK_GBS_PER_DIR, "share_of_step": ar_us * 1e-3 / ms,
+                "nccl_algo": os.environ.get("NCCL_ALGO", "auto"), "nccl_proto": os.environ.get("NCCL_PROTO", "auto"),
+                "note": "latency-bound: 178,560 B per step (SURVEY §8(e))"}
+
+    kt = wl.kernel_times(args.kernel_reps) if args.kernel_reps > 0 else []
     kernel_sum_ms = sum(k["ms"] for k in kt)
     dom = max(kt, key=lambda k: k["ms"]) if kt else dict(layer="-", pass_="-", ms=float("nan"), bytes=0,
                                                          gbs=float("nan"))
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(peaks_path):
-        with open(peaks_path) as f:
-            peak = float(json.load(f)["hbm_gbs"])
-        peak_src = "measured"
-    else:
-        peak, peak_src = FALLBACK_HBM_GBS, "fallback"
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
                 tr = json.load(f)
-            key = f"{args.alpha:g}/{args.res}/{args.batch}/{args.dtype}/{args.layout}/{dom['layer']}/{dom['pass_']}"
+            key = f"{args.alpha:g}/{args.res}/{batch}/{args.dtype}/{args.layout}/{dom['layer']}/{dom['pass_']}"
             traffic = tr.get(key)
         except Exception:
             traffic = None
@@ -451,70 +606,79 @@ def main():
     # ---- end to end through the public binding with host buffers (pinned), eager calls
     e2e = None
     if args.e2e_steps > 0:
-        host_in = []
-        for b in bufs:
-            host_in.append((b["x"].cpu().pin_memory(), b["dy"].cpu().pin_memory(), b["w"].cpu().pin_memory()))
-        host_dw = torch.empty(dw_bucket.shape, dtype=torch.float32).pin_memory()
+        s0 = wl.sets[0]
+        host_in = [(b["x"].cpu().pin_memory(), b["dy"].cpu().pin_memory(), w.cpu().pin_memory())
+                   for b, w in zip(s0, wl.w)]
+        host_dw = torch.empty(wl.bucket.flat.shape, dtype=torch.float32).pin_memory()
         h2d = sum(t.numel() * t.element_size() for tup in host_in for t in tup)
         d2h = host_dw.numel() * 4
 
         def e2e_step():
-            for b, (hx, hdy, hw) in zip(bufs, host_in):
+            for b, w, (hx, hdy, hw) in zip(s0, wl.w, host_in):
                 b["x"].copy_(hx, non_blocking=True)
                 b["dy"].copy_(hdy, non_blocking=True)
-                b["w"].copy_(hw, non_blocking=True)
-            step_kernels()
+                w.copy_(hw, non_blocking=True)
+            wl.step_kernels(0)
             if world > 1:
-                bucket.allreduce()
-            host_dw.copy_(dw_bucket, non_blocking=True)
+                wl.bucket.allreduce()
+            host_dw.copy_(wl.bucket.flat, non_blocking=True)
 
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(wl.stream):
             e2e_step()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            f0.record(stream)
+            f0.record(wl.stream)
             for _ in range(args.e2e_steps):
                 e2e_step()
-            f1.record(stream)
+            f1.record(wl.stream)
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
         if world > 1:
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": images / (e2e_ms / 1000.0), "unit": "images/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": total_images / (e2e_ms / 1000.0), "unit": "images/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": args.e2e_steps,
                "path": "python binding -> C ABI eager calls; pinned host->device copies of x, dy, w for all "
                        "13 layers and device->host copy of the dw bucket inside the timed region"}
 
+    gpu_launches = len(wl.kernel_list()) * args.steps
+    plans_note = wl.plans_note()
+    footprint = wl.footprint
+    nfused = sum(wl.fused)
+    del wl
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    # ---- the >= 70 % target set at batch 128 (N=1 only; each its own tuned, graph-replayed step)
+    b128 = None
+    if world == 1 and not args.no_b128 and not args.plans:
+        b128 = [b128_workload(torch, dev, dt, lay, args.b128_steps, peak) for dt, lay in B128_SET]
+
     # ---- CPU baseline (oracle), rank 0 at N=1 only
-    cpu = None
+    cpu = cpu_all = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        v, nimg, secs = oracle_sample(layers_for(args, 1), args.cpu_seconds)
-        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle",
-               "sample": f"{nimg} images of the 13-layer stack (fwd+bwd_data+bwd_filter), plain-C fp64 oracle, "
-                         f"single thread, {secs:.1f} s"}
+        cpu, cpu_all = cpu_baselines(layers_for(args.alpha, args.res, 1), args.cpu_seconds)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded torch U[-1,1] on device; parity tests use the splitmix64 generator)",
-            "config": {"workload": workload_name(args), "global_batch": images, "batch_per_gpu": args.batch,
-                       "layers": 13, "layout": args.layout, "parallelism": f"dp{world}",
-                       "l2": f"no flush: step footprint {footprint / 1e9:.2f} GB >> 126 MB L2",
-                       "graph": graph is not None,
+            "config": {"workload": workload_name(args.alpha, args.res), "global_batch": total_images,
+                       "batch_per_gpu": batch, "layers": 13, "layout": args.layout, "parallelism": f"dp{world}",
+                       "l2": f"no flush: two input sets alternate between steps, each step's footprint "
+                             f"{footprint / Workload.NSETS / 1e9:.2f} GB >> 126 MB L2",
+                       "graph": not args.no_graph,
                        "schedule": ("serial" if args.serial else "bwd_filter on a side stream (overlaps bwd_data)") +
-                                   f"; fused backward on {sum(b['fused'] for b in bufs)}/13 layers",
-                       "plans": ("planner defaults" if not tuned else
-                                 "measured selection (tune.py, before the timed region): "
-                                 f"{sum(1 for t in tuned.values() for v in t.values() if v['index'] != 0)} of "
-                                 f"{sum(len(t) for t in tuned.values())} tuned passes changed")},
-            "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / world / peak,
-            "algorithmic_bytes_per_step": sbytes * world,
+                                   f"; fused backward on {nfused}/13 layers",
+                       "plans": plans_note, "dev_env": dev_env()},
+            "step_ms": {"p10": pct(per, 10), "p50": pct(per, 50), "p90": pct(per, 90), "mean": ms_local},
+            "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / world / peak, "hbm_frac_of_8tbs": hbm_gbs / world / NOMINAL_HBM_GBS,
+            "algorithmic_bytes_per_step": sbytes,
             "roofline": ({"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
                           "frac": dom["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
                           "kernel": f"{dom['layer']}/{dom['pass_']}", "ms": dom["ms"], "bytes": dom["bytes"],
@@ -524,11 +688,13 @@ def main():
             "clocks": sampler.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": len(kernels) * args.steps,
+            "cpu_baseline_all_cores": cpu_all,
+            "comm": comm,
+            "workloads_b128": b128,
+            "gpu_launches": gpu_launches,
             "paper_context": {"img_s": PAPER_CONTEXT_IMG_S, "hw": "GTX 1080 Ti, Caffe, Table III (context only)"},
         }
         if args.extra:
-            line["tuning"] = tuned
             line["kernels"] = [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in kk.items()} for kk in kt]
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle (gcc -O2 -ffp-contract=off, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fopenmp",
                                "-fPIC", "-shared", _SRC, "-o", tmp, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
@@ -63,8 +63,22 @@ def _load():
         lib.oracle_round.argtypes = [dp, dp, i64, i32]
         lib.oracle_out_size.argtypes = [i64, i32, i32, i32, ctypes.POINTER(i64)]
         lib.oracle_out_size.restype = i32
+        lib.oracle_set_threads.argtypes = [i32]
+        lib.oracle_set_threads.restype = None
+        lib.oracle_get_threads.argtypes = []
+        lib.oracle_get_threads.restype = i32
         _lib = lib
     return _lib
+
+
+def set_threads(t: int) -> None:
+    """Outer-loop OpenMP threads for fwd / bwd_data / bwd_filter (1 = sequential, the default).  Every
+    output element is still summed by one thread in definition order: results are bitwise unchanged."""
+    _load().oracle_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return int(_load().oracle_get_threads())
 
 
 def _p(a: np.ndarray):

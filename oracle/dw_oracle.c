@@ -8,7 +8,11 @@
  * path (paper_1803_09926_b200/csrc); neither includes the other.
  *
  * Everything is double precision, nested loops in definition order, no
- * blocking, no fusion, single-threaded.  Every product of two
+ * blocking, no fusion, single-threaded by default.  For the
+ * all-cores CPU baseline oracle_set_threads(t > 1) splits
+ * the OUTER loops (images x channels for a1/a2, output channels for a3) over t
+ * OpenMP threads; each output element is still summed by one thread in the same
+ * order, so results are bitwise identical to the single-thread run (tested).  Every product of two
  * fp32 (or bf16) inputs is exact in double, so the only error is the double
  * summation, <= (n-1) * 2^-53 * sum|t|.  Each function also
  * returns, per output element, the sum of |terms| that the parity tolerance is
@@ -40,6 +44,11 @@
 #define ORACLE_NCHW 0
 #define ORACLE_NHWC 1
 
+/* Threads for the outer loops (1 = the plain sequential oracle). */
+static int oracle_nthreads = 1;
+void oracle_set_threads(int t) { oracle_nthreads = t < 1 ? 1 : t; }
+int oracle_get_threads(void) { return oracle_nthreads; }
+
 /* Flat offset of logical element (n, c, h, w) of a tensor with C channels and
  * H x W spatial size in the given layout. */
 static size_t at(int layout, int64_t C, int64_t H, int64_t W,
@@ -66,6 +75,7 @@ void oracle_dw_fwd(const double* x, const double* wt, double* y, double* abs_y,
   int64_t Ho, Wo;
   if (!oracle_out_size(H, kh, sh, ph, &Ho) || !oracle_out_size(W, kw, sw, pw, &Wo)) return;
   int64_t Co = C * m;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1) num_threads(oracle_nthreads) if (oracle_nthreads > 1)
   for (int64_t n = 0; n < N; ++n)
     for (int64_t c = 0; c < C; ++c)
       for (int j = 0; j < m; ++j) {
@@ -99,6 +109,7 @@ void oracle_dw_bwd_data(const double* dy, const double* wt, double* dx, double* 
   int64_t Ho, Wo;
   if (!oracle_out_size(H, kh, sh, ph, &Ho) || !oracle_out_size(W, kw, sw, pw, &Wo)) return;
   int64_t Co = C * m;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1) num_threads(oracle_nthreads) if (oracle_nthreads > 1)
   for (int64_t n = 0; n < N; ++n)
     for (int64_t c = 0; c < C; ++c)
       for (int64_t ih = 0; ih < H; ++ih)
@@ -133,6 +144,7 @@ void oracle_dw_bwd_filter(const double* x, const double* dy, double* dw, double*
   int64_t Ho, Wo;
   if (!oracle_out_size(H, kh, sh, ph, &Ho) || !oracle_out_size(W, kw, sw, pw, &Wo)) return;
   int64_t Co = C * m;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1) num_threads(oracle_nthreads) if (oracle_nthreads > 1)
   for (int64_t c = 0; c < C; ++c)
     for (int j = 0; j < m; ++j) {
       int64_t o = c * m + j;

@@ -12,6 +12,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifdef DWCONV_DEV_KNOBS
+#include <cstdlib>
+#endif
+
+// Launch-shape overrides for kernel development (DWCONV_FD_FORCE, DWCONV_BF_FORCE,
+// ...) read the environment only in a build compiled with -DDWCONV_DEV_KNOBS.  The
+// shipped library (build.py) never reads them, so no environment variable can
+// change what a call launches.
+static inline const char* dev_knob(const char* name) {
+#ifdef DWCONV_DEV_KNOBS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 namespace dwk {
 
 // ------------------------------------------------------------------ elements

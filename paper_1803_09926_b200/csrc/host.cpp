@@ -90,7 +90,9 @@ int check_ptr(const void* p, int64_t elems, int eb) {
 
 int check_device(DevInfo* di) {
   if (!dev_info(di)) return DWCONV_ERR_CUDA;
-  if (di->major != 10) return DWCONV_ERR_UNSUPPORTED;  // built for sm_100a only
+  // the library carries only an sm_100a cubin (no PTX): other 10.x parts (sm_103)
+  // cannot load it, so they are UNSUPPORTED rather than a later launch failure
+  if (di->major != 10 || di->minor != 0) return DWCONV_ERR_UNSUPPORTED;
   return DWCONV_OK;
 }
 
@@ -486,7 +488,12 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
     // the planner's own pick (what an unselected call launches) leads the list
     Plan dp;
     make_plan_uncached(g, pass, di, &dp);
-    if (dp.variant == DWCONV_VARIANT_NCHW_CHUNK) cands.push_back(dp.chunk);
+    // candidate 0 is the planner's own pick; when that is not a chunk-family plan
+    // (generic kernel, or bf16 fused backward = the two separate calls) there is
+    // no list (the header's "0 candidates"), so index 0 never names a plan the
+    // planner rejected
+    if (dp.variant != DWCONV_VARIANT_NCHW_CHUNK) return DWCONV_OK;
+    cands.push_back(dp.chunk);
     if (pass == DWCONV_PASS_BWD_FILTER && g.dtype <= DWCONV_BF16) {
       // band bwd_filter for large planes: {warps, ring slots, band rows}
       // {warps, ring slots, band rows, planes per warp}
@@ -541,6 +548,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         if (!dup) cands.push_back(c);
       }
     }
+    if ((int)cands.size() > DWCONV_MAX_CANDIDATES) cands.resize(DWCONV_MAX_CANDIDATES);
     std::vector<Plan> wrapped;
     for (const ChunkPlan& c : cands) {
       Plan q;

@@ -48,7 +48,6 @@ struct NArgs {
   FastDiv div_ncg, div_nsb, div_m, div_co;
   FastDiv div_c, div_nb;  // channel of a plane index; chunk -> (plane, band)
   int wbulk;              // w is 16-B aligned with a 16-B multiple size: weight rows may be bulk-copied
-  int dbg;                // tuning aid (DWCONV_DEBUG): 1 = skip compute, 2 = skip stores
   int early_pdl;          // persistent kernels: trigger the dependent launch once the producer is done
 };
 

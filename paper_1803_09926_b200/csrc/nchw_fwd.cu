@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
       const T* swr = reinterpret_cast<const T*>(swc) + ww.off;  // raw rows (ww.tma)
       if constexpr (PAIR) {
         const int npair = (npl + 1) >> 1;
-        const int ntp = (a.dbg & 1) ? 0 : npair * a.nsb * ncg;
+        const int ntp = npair * a.nsb * ncg;
         for (int t = ctid; t < ntp; t += nct) {
           const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
           const int c0 = (t - t2 * ncg) * V;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
           T* yob = yoa + (int64_t)a.Ho * Wo;
 #pragma unroll
           for (int tt = 0; tt < R; ++tt) {
-            if (oh0 + tt < k.r1 && !(a.dbg & 2)) {
+            if (oh0 + tt < k.r1) {
               float va[V], vb[V];
 #pragma unroll
               for (int u = 0; u < V; ++u) { va[u] = acc[tt][u].x; vb[u] = acc[tt][u].y; }
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
           }
         }
       }
-      const int ntiles = ((a.dbg & 1) || PAIR) ? 0 : npl * a.nsb * ncg;
+      const int ntiles = PAIR ? 0 : npl * a.nsb * ncg;
       for (int t = ctid; t < ntiles; t += nct) {
         const int t2 = (int)fdiv((uint32_t)t, a.div_ncg);
         const int c0 = (t - t2 * ncg) * V;
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
         T* yo = y + ((k.q0 * m + pp) * a.Ho + oh0) * Wo + c0;
 #pragma unroll
         for (int tt = 0; tt < R; ++tt)
-          if (oh0 + tt < k.r1 && !(a.dbg & 2)) VecIO<T, V>::store(yo + tt * Wo, acc[tt]);
+          if (oh0 + tt < k.r1) VecIO<T, V>::store(yo + tt * Wo, acc[tt]);
       }
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);

@@ -27,7 +27,7 @@ int64_t gcd64(int64_t a, int64_t b) {
 }
 
 int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* e = std::getenv(name);
+  const char* e = dev_knob(name);
   const int v = e ? std::atoi(e) : dflt;
   return (v >= lo && v <= hi) ? v : dflt;
 }
@@ -312,7 +312,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       // tuning aid: DWCONV_FD_FORCE="T,P,band_rows" (band_rows 0 = whole planes) pins the chunk shape
       static const int* force = []() -> const int* {
         static int f[3];
-        const char* e = getenv("DWCONV_FD_FORCE");
+        const char* e = dev_knob("DWCONV_FD_FORCE");
         if (!e || sscanf(e, "%d,%d,%d", &f[0], &f[1], &f[2]) != 3) return nullptr;
         return f;
       }();
@@ -429,7 +429,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   // tuning aid: DWCONV_BF_FORCE="P,tpg,nsb" pins the chunk shape (nsb = strip rows per band, 0 = whole planes)
   static const int* bf_force = []() -> const int* {
     static int f[3];
-    const char* e = getenv("DWCONV_BF_FORCE");
+    const char* e = dev_knob("DWCONV_BF_FORCE");
     if (!e || sscanf(e, "%d,%d,%d", &f[0], &f[1], &f[2]) != 3) return nullptr;
     return f;
   }();
@@ -581,8 +581,6 @@ static nchw::NArgs base_args(const Geom& g, const ChunkPlan& p) {
   a.div_m = make_fastdiv((uint32_t)g.m);
   a.div_co = make_fastdiv((uint32_t)a.Co);
   a.div_c = make_fastdiv((uint32_t)g.C);
-  static const int dbg = nchw::env_int("DWCONV_DEBUG", 0, 0, 3);
-  a.dbg = dbg;
   static const int early = nchw::env_int("DWCONV_EARLY_PDL", 1, 0, 1);
   a.early_pdl = early;
   a.div_nb = make_fastdiv((uint32_t)std::max(1, p.nbands));

@@ -1084,7 +1084,7 @@ SKernelFn kernel_for(int dtype, int pass, int W, int S = 1) {
 }
 
 int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* e = std::getenv(name);
+  const char* e = dev_knob(name);
   const int v = e ? std::atoi(e) : dflt;
   return (v >= lo && v <= hi) ? v : dflt;
 }

@@ -321,7 +321,7 @@ HKernelFn bf_pick_k(int K, int S) {
 
 static cudaError_t launch(HKernelFn fn, int grid, int smem, cudaStream_t st, const HArgs& a) {
   static const bool pdl = []() {
-    const char* e = std::getenv("DWCONV_PDL");
+    const char* e = dev_knob("DWCONV_PDL");
     return !(e && e[0] == '0');
   }();
   cudaLaunchConfig_t cfg = {};
@@ -406,7 +406,7 @@ bool plan_nhwc(const Geom& g, int pass, int num_sms, NhwcPlan* p) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem) != cudaSuccess || occ < 1) return false;
   // slices: ~one wave of CTAs (measured best: each CTA's epilogue is a fixed cost),
   // and <= 120 blocks per thread (running-sum chain)
-  static const int waves = []() { const char* e = std::getenv("DWCONV_NHWC_BF_WAVES"); return e ? std::max(1, std::atoi(e)) : 1; }();
+  static const int waves = []() { const char* e = dev_knob("DWCONV_NHWC_BF_WAVES"); return e ? std::max(1, std::atoi(e)) : 1; }();
   int64_t nsl = std::max<int64_t>(1, ((int64_t)waves * occ * num_sms + groups - 1) / groups);
   nsl = std::max<int64_t>(nsl, (rows * bpr + (int64_t)PSET * 120 - 1) / ((int64_t)PSET * 120));
   nsl = std::min<int64_t>(nsl, std::min<int64_t>(rows, 256));

@@ -498,7 +498,7 @@ bool allow_max_smem(const void* fn, int smem_optin) {
 }
 
 int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* e = std::getenv(name);
+  const char* e = dev_knob(name);
   const int v = e ? std::atoi(e) : dflt;
   return (v >= lo && v <= hi) ? v : dflt;
 }

@@ -82,18 +82,59 @@ def _check_dev(*ts: torch.Tensor) -> None:
     for t in ts:
         if not t.is_cuda:
             raise ValueError("dwconv tensors must be CUDA device tensors (there is no CPU path)")
+    devs = {t.device for t in ts}
+    if len(devs) > 1:
+        raise ValueError(f"dwconv tensors must share one device, got {sorted(str(v) for v in devs)}")
+
+
+_STORAGE = {F32: torch.float32, BF16: torch.bfloat16}
+
+
+def _check_tensors(d: Desc, **ts: torch.Tensor) -> None:
+    """Match every tensor against the descriptor before its raw pointer reaches the C library (which sees
+    no shapes or dtypes): storage dtype, logical [N, C, H, W] / [N, C*m, Ho, Wo] shape, memory format and
+    weight size.  A mismatch raises ValueError naming both shapes (SPEC "shape mismatch" is an error)."""
+    _check_dev(*ts.values())
+    ho, wo = output_shape(d)
+    co = d.c * d.multiplier
+    want = {"x": (d.n, d.c, d.h, d.w), "dx": (d.n, d.c, d.h, d.w), "y": (d.n, co, ho, wo), "dy": (d.n, co, ho, wo)}
+    sdt = _STORAGE[d.dtype]
+    for name, t in ts.items():
+        if name == "dw":
+            if t.dtype != torch.float32:
+                raise TypeError("dw is always float32")
+            if t.numel() != co * d.kh * d.kw or not t.is_contiguous():
+                raise ValueError(f"dw must be a contiguous float32 tensor of {co * d.kh * d.kw} elements "
+                                 f"([C*m, kh, kw] = [{co}, {d.kh}, {d.kw}]), got shape {tuple(t.shape)}")
+            continue
+        if t.dtype != sdt:
+            raise TypeError(f"{name} has dtype {t.dtype} but the descriptor's storage dtype is {sdt}")
+        if name == "w":
+            if t.numel() != co * d.kh * d.kw or not t.is_contiguous():
+                raise ValueError(f"w must be a contiguous tensor of {co * d.kh * d.kw} elements "
+                                 f"([C*m, kh, kw] = [{co}, {d.kh}, {d.kw}]), got shape {tuple(t.shape)}")
+            continue
+        if tuple(t.shape) != want[name]:
+            raise ValueError(f"{name} has shape {tuple(t.shape)} but the descriptor needs {want[name]}")
+        ok = t.is_contiguous() if d.layout == NCHW else t.is_contiguous(memory_format=torch.channels_last)
+        if not ok:
+            raise ValueError(f"{name} is not contiguous in the descriptor's layout "
+                             f"({'NCHW' if d.layout == NCHW else 'NHWC / channels_last'})")
 
 
 # ----------------------------------------------------------------- raw C mirrors
 def dwconv_fwd(d: Desc, x: torch.Tensor, w: torch.Tensor, y: torch.Tensor, stream=None) -> None:
-    _check_dev(x, w, y)
-    _lib.check(_lib.load().dwconv_fwd(ctypes.byref(d), _ptr(x), _ptr(w), _ptr(y), _stream(stream)), "dwconv_fwd")
+    _check_tensors(d, x=x, w=w, y=y)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.load().dwconv_fwd(ctypes.byref(d), _ptr(x), _ptr(w), _ptr(y), _stream(stream)),
+                   "dwconv_fwd")
 
 
 def dwconv_bwd_data(d: Desc, dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, stream=None) -> None:
-    _check_dev(dy, w, dx)
-    _lib.check(_lib.load().dwconv_bwd_data(ctypes.byref(d), _ptr(dy), _ptr(w), _ptr(dx), _stream(stream)),
-               "dwconv_bwd_data")
+    _check_tensors(d, dy=dy, w=w, dx=dx)
+    with torch.cuda.device(dy.device):
+        _lib.check(_lib.load().dwconv_bwd_data(ctypes.byref(d), _ptr(dy), _ptr(w), _ptr(dx), _stream(stream)),
+                   "dwconv_bwd_data")
 
 
 def dwconv_bwd_filter_workspace_bytes(d: Desc) -> int:
@@ -102,12 +143,11 @@ def dwconv_bwd_filter_workspace_bytes(d: Desc) -> int:
 
 def dwconv_bwd_filter(d: Desc, x: torch.Tensor, dy: torch.Tensor, dw: torch.Tensor,
                       workspace: Optional[torch.Tensor], stream=None) -> None:
-    _check_dev(x, dy, dw)
-    if dw.dtype != torch.float32:
-        raise TypeError("dw is always float32")
+    _check_tensors(d, x=x, dy=dy, dw=dw)
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    _lib.check(_lib.load().dwconv_bwd_filter(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(dw), _ptr(workspace),
-                                             nbytes, _stream(stream)), "dwconv_bwd_filter")
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.load().dwconv_bwd_filter(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(dw), _ptr(workspace),
+                                                 nbytes, _stream(stream)), "dwconv_bwd_filter")
 
 
 def dwconv_bwd_workspace_bytes(d: Desc) -> int:
@@ -117,12 +157,11 @@ def dwconv_bwd_workspace_bytes(d: Desc) -> int:
 def dwconv_bwd(d: Desc, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, dw: torch.Tensor,
                workspace: Optional[torch.Tensor], stream=None) -> None:
     """Fused backward: dx and dw from one pass over x and dy where the library has a fused kernel."""
-    _check_dev(x, dy, w, dx, dw)
-    if dw.dtype != torch.float32:
-        raise TypeError("dw is always float32")
+    _check_tensors(d, x=x, dy=dy, w=w, dx=dx, dw=dw)
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    _lib.check(_lib.load().dwconv_bwd(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(w), _ptr(dx), _ptr(dw),
-                                      _ptr(workspace), nbytes, _stream(stream)), "dwconv_bwd")
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.load().dwconv_bwd(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(w), _ptr(dx), _ptr(dw),
+                                          _ptr(workspace), nbytes, _stream(stream)), "dwconv_bwd")
 
 
 def dwconv_workspace_init(workspace: torch.Tensor, stream=None) -> None:

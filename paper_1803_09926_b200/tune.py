@@ -27,6 +27,10 @@ PASSES = {"fwd": PASS_FWD, "bwd_data": PASS_BWD_DATA, "bwd_filter": PASS_BWD_FIL
 
 
 def _graph_us(calls, reps: int, stream: torch.cuda.Stream) -> float:
+    # the tensor copies and the zero-filled workspace were made on the caller's
+    # stream: order the timing stream after them (the bwd_filter tickets must
+    # read as zero on the first launch)
+    stream.wait_stream(torch.cuda.current_stream(stream.device))
     with torch.cuda.stream(stream):
         for c in calls:
             c()

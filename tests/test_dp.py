@@ -18,7 +18,7 @@ import synth
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
-from dp_worker import LAYERS, global_inputs  # noqa: E402
+from dp_worker import LAYERS, MOBILENET, global_inputs  # noqa: E402
 
 from paper_1803_09926_b200 import dp  # noqa: E402
 
@@ -59,11 +59,9 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("batch", [6, 5, 1])  # even, ragged, one rank empty
-def test_gloo_world2_allreduce_equals_full_batch(tmp_path, batch):
-    out = str(tmp_path / "bucket.npy")
+def _run_world2(out, batch, mode="oracle"):
     env = dict(os.environ, WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
-    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "dp_worker.py"), out, str(batch)],
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "dp_worker.py"), out, str(batch), mode],
                               env=dict(env, RANK=str(r)), stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
              for r in range(2)]
     logs = []
@@ -74,7 +72,12 @@ def test_gloo_world2_allreduce_equals_full_batch(tmp_path, batch):
             p.kill()
             raise
     assert all(p.returncode == 0 for p in procs), "\n".join(logs)
-    flat = np.load(out)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("batch", [6, 5, 1])  # even, ragged, one rank empty
+def test_gloo_world2_allreduce_equals_full_batch(tmp_path, batch):
+    flat = _run_world2(str(tmp_path / "bucket.npy"), batch)
     ref = dp.DwBucket([(L.c * L.m, L.k, L.k) for L in LAYERS], device="cpu")
     for i, L in enumerate(LAYERS):
         x, dy = global_inputs(L, i, batch)
@@ -106,3 +109,29 @@ def test_gpu_batch_shards_sum_to_full_batch():
             bucket.views[0].add_(dwl.bwd_filter(x[s:s + c].contiguous(), dy[s:s + c].contiguous(), wshape, L.s, L.p))
         torch.cuda.synchronize()
         assert torch.equal(bucket.views[0], full), L
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["int", "unif"])
+@pytest.mark.parametrize("batch", [6, 5])  # even, ragged
+def test_gpu_world2_cuda_dw_allreduce_equals_oracle_global_batch(tmp_path, batch, kind):
+    """Row a6 end to end through the product path (R6): two processes on one GPU, each runs
+    dwconv_bwd_filter on its batch shard into the CUDA DwBucket, DwBucket.allreduce over gloo; the reduced
+    bucket must equal the oracle's dw of the GLOBAL batch -- bitwise on small integers (P6/P8), within the
+    fp32 bound plus one rounding per rank partial on uniform data (R6)."""
+    flat = _run_world2(str(tmp_path / "bucket.npy"), batch, "cuda-int" if kind == "int" else "cuda")
+    layers = LAYERS + MOBILENET
+    ref = dp.DwBucket([(L.c * L.m, L.k, L.k) for L in layers], device="cpu")
+    for i, L in enumerate(layers):
+        x, dy = global_inputs(L, i, batch, kind)
+        dwv, absum = oracle.bwd_filter(x, dy, (L.c * L.m, L.k, L.k), L.s, L.p)
+        got = flat[ref.offsets[i]:ref.offsets[i] + dwv.size].reshape(dwv.shape)
+        if kind == "int":
+            assert np.array_equal(got, dwv.astype(np.float32)), L
+        else:
+            tol = 1e-5 * absum + 2 * 2.0 ** -24 * np.abs(dwv)
+            assert np.all(np.abs(got - dwv) <= tol), (L, np.max(np.abs(got - dwv) - tol))
+    mask = np.ones(flat.size, bool)
+    for i, L in enumerate(layers):
+        mask[ref.offsets[i]:ref.offsets[i] + L.c * L.m * L.k * L.k] = False
+    assert np.all(flat[mask] == 0)

@@ -31,11 +31,31 @@ def _dev(a, dtype, layout=NCHW):
     return t.contiguous(memory_format=torch.channels_last) if (layout == NHWC and t.dim() == 4) else t
 
 
-def _check_layer(L, dtype, amax, seed, layout=NCHW):
+def _inputs(L, dtype, kind, amax, seed):
+    shapes = ((L.n, L.c, L.h, L.w), (L.c * L.m, L.k, L.k), (L.n, L.c * L.m, L.ho, L.wo))
+    if kind == "int":
+        return [synth.integers(seed * 10 + i + 1, shp, amax) for i, shp in enumerate(shapes)]
+    return [synth.uniform(seed * 10 + i + 1, shp, dtype) for i, shp in enumerate(shapes)]
+
+
+def _cmp(got, ref, absum, dtype, kind, tag):
+    """R1 (integers: bitwise) or R2 / R3 (uniform: |gpu - ref| <= 1e-5 sum|t| (+ 1e-2 |ref| for bf16 storage),
+    exact zero where every term is zero)."""
+    if kind == "int":
+        assert np.array_equal(got, ref.astype(np.float32)), tag
+        return
+    tol = 1e-5 * absum + (1e-2 * np.abs(ref) if dtype == "bf16" else 0.0)
+    err = np.abs(got.astype(np.float64) - ref)
+    assert np.all(err <= tol), f"{tag}: {int((err > tol).sum())} outside, worst {np.max(err - tol):.3e}"
+    assert np.all(got[absum == 0] == 0), tag
+
+
+def _check_layer(L, dtype, amax, seed, layout=NCHW, kind="int"):
+    """Every candidate plan of every pass of layer L (and the fused backward where the library has it)
+    against oracle outputs computed one by one on sampled (n, c) planes / dw channels (any m, K, s)."""
     rng = np.random.default_rng(seed)
-    x = synth.integers(seed * 10 + 1, (L.n, L.c, L.h, L.w), amax)
-    w = synth.integers(seed * 10 + 2, (L.c * L.m, L.k, L.k), amax)
-    dy = synth.integers(seed * 10 + 3, (L.n, L.c * L.m, L.ho, L.wo), amax)
+    x, w, dy = _inputs(L, dtype, kind, amax, seed)
+    m = L.m
     d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout, F32 if dtype == "f32" else BF16)
     xd, wd, dyd = _dev(x, dtype, layout), _dev(w, dtype), _dev(dy, dtype, layout)
     y = torch.empty_like(dyd)
@@ -45,18 +65,33 @@ def _check_layer(L, dtype, amax, seed, layout=NCHW):
     chans = sorted({int(c) for c in rng.integers(L.c, size=NSAMP)})
     s, p = L.s, L.p
     ref = {"fwd": {}, "bwd_data": {}, "bwd_filter": {}}
+    f64 = np.float64
     for n, c in planes:
-        ref["fwd"][(n, c)] = oracle.fwd(x[n:n + 1, c:c + 1].astype(np.float64),
-                                        w[c:c + 1].astype(np.float64), s, p)[0][0, 0]
-        ref["bwd_data"][(n, c)] = oracle.bwd_data(dy[n:n + 1, c:c + 1].astype(np.float64),
-                                                  w[c:c + 1].astype(np.float64), (1, 1, L.h, L.w), s, p)[0][0, 0]
+        wc = w[c * m:(c + 1) * m].astype(f64)
+        yv, ya = oracle.fwd(x[n:n + 1, c:c + 1].astype(f64), wc, s, p)
+        ref["fwd"][(n, c)] = (yv[0], ya[0])
+        dv, da = oracle.bwd_data(dy[n:n + 1, c * m:(c + 1) * m].astype(f64), wc, (1, 1, L.h, L.w), s, p)
+        ref["bwd_data"][(n, c)] = (dv[0, 0], da[0, 0])
     for c in chans:
-        ref["bwd_filter"][c] = oracle.bwd_filter(x[:, c:c + 1].astype(np.float64), dy[:, c:c + 1].astype(np.float64),
-                                                 (1, L.k, L.k), s, p)[0][0]
+        ref["bwd_filter"][c] = oracle.bwd_filter(x[:, c:c + 1].astype(f64), dy[:, c * m:(c + 1) * m].astype(f64),
+                                                 (m, L.k, L.k), s, p)
+
+    def check_y(tag):
+        for (n, c), (r, a) in ref["fwd"].items():
+            _cmp(y[n, c * m:(c + 1) * m].float().cpu().numpy(), r, a, dtype, kind, tag)
+
+    def check_dx(tag):
+        for (n, c), (r, a) in ref["bwd_data"].items():
+            _cmp(dx[n, c].float().cpu().numpy(), r, a, dtype, kind, tag)
+
+    def check_dw(tag):
+        got = dwt.cpu().numpy()
+        for c, (r, a) in ref["bwd_filter"].items():
+            _cmp(got[c * m:(c + 1) * m], r, a, "f32", kind, tag)
+
     for name, pas in (("fwd", 0), ("bwd_data", 1), ("bwd_filter", 2)):
         cands = ops.dwconv_plan_candidates(d, pas)
         if not cands:  # shapes only the generic kernels cover: check the default path once
-            assert layout == NHWC or L.c < 4 or L.n == 0, f"{L.name} {name}: no candidates"
             cands = [None]
         ws = None
         if pas == 2:
@@ -67,43 +102,37 @@ def _check_layer(L, dtype, amax, seed, layout=NCHW):
             for i, cand in enumerate(cands):
                 if cand is not None:
                     ops.dwconv_plan_select(d, pas, i)
-                tag = f"{L.name} {dtype} {name} candidate {i} {cand}"
+                tag = f"{L.name} {dtype} {kind} {name} candidate {i} {cand}"
                 if pas == 0:
                     y.fill_(float("nan"))
                     ops.dwconv_fwd(d, xd, wd, y)
-                    for (n, c), r in ref["fwd"].items():
-                        got = y[n, c].float().cpu().numpy()
-                        assert np.array_equal(got, r.astype(np.float32)), tag
+                    check_y(tag)
                 elif pas == 1:
                     dx.fill_(float("nan"))
                     ops.dwconv_bwd_data(d, dyd, wd, dx)
-                    for (n, c), r in ref["bwd_data"].items():
-                        got = dx[n, c].float().cpu().numpy()
-                        assert np.array_equal(got, r.astype(np.float32)), tag
+                    check_dx(tag)
                 else:
                     dwt.fill_(float("nan"))
                     ops.dwconv_bwd_filter(d, xd, dyd, dwt, ws)
-                    got = dwt.cpu().numpy()
-                    for c, r in ref["bwd_filter"].items():
-                        assert np.array_equal(got[c], r.astype(np.float32)), tag
+                    check_dw(tag)
         finally:
             ops.dwconv_plan_select(d, pas, -1)
     # fused backward (dwconv_bwd: dx and dw from one pass) where the library has it
-    if layout == NCHW and ops.dwconv_plan(d, 3)["variant_name"] != "none":
-        cands = ops.dwconv_plan_candidates(d, 3)
-        ws = torch.zeros(max(16, max(c["workspace_bytes"] for c in cands)), dtype=torch.uint8, device="cuda")
+    if ops.dwconv_plan(d, 3)["variant_name"] != "none":
+        cands = ops.dwconv_plan_candidates(d, 3) or [None]
+        ws = torch.zeros(max(16, ops.dwconv_bwd_workspace_bytes(d),
+                             max((c["workspace_bytes"] for c in cands if c), default=0)),
+                         dtype=torch.uint8, device="cuda")
         try:
             for i, cand in enumerate(cands):
-                ops.dwconv_plan_select(d, 3, i)
-                tag = f"{L.name} {dtype} bwd (fused) candidate {i} {cand}"
+                if cand is not None:
+                    ops.dwconv_plan_select(d, 3, i)
+                tag = f"{L.name} {dtype} {kind} bwd (fused) candidate {i} {cand}"
                 dx.fill_(float("nan"))
                 dwt.fill_(float("nan"))
                 ops.dwconv_bwd(d, xd, dyd, wd, dx, dwt, ws)
-                for (n, c), r in ref["bwd_data"].items():
-                    assert np.array_equal(dx[n, c].float().cpu().numpy(), r.astype(np.float32)), tag
-                got = dwt.cpu().numpy()
-                for c, r in ref["bwd_filter"].items():
-                    assert np.array_equal(got[c], r.astype(np.float32)), tag
+                check_dx(tag)
+                check_dw(tag)
         finally:
             ops.dwconv_plan_select(d, 3, -1)
     torch.cuda.synchronize()
@@ -127,6 +156,46 @@ def test_candidates_fullsize_nhwc(layer, dtype):
 def test_candidates_fullsize_b128_bf16(layer):
     L = [l for l in synth.mobilenet_v1_dw(128) if l.name == layer][0]
     _check_layer(L, "bf16", 2, seed=8)
+
+
+@pytest.mark.parametrize("layer", [L.name for L in synth.mobilenet_v1_dw(64)])
+def test_candidates_fullsize_b64_fp32_uniform(layer):
+    """Random U[-1,1] data at the bench's size (configs[1]) over every tuned candidate: R2 on the sampled
+    outputs, i.e. the rounding of the full 802,816-term dw sums, not only their indexing."""
+    L = [l for l in synth.mobilenet_v1_dw(64) if l.name == layer][0]
+    _check_layer(L, "f32", 0, seed=17, kind="unif")
+
+
+@pytest.mark.parametrize("layout", [NCHW, NHWC])
+@pytest.mark.parametrize("layer", [L.name for L in synth.mobilenet_v1_dw(128)])
+def test_candidates_fullsize_b128_bf16_uniform(layer, layout):
+    """bf16 storage, U[-1,1], batch 128 (the >= 70 % target set): R3 over every candidate, both layouts."""
+    L = [l for l in synth.mobilenet_v1_dw(128) if l.name == layer][0]
+    _check_layer(L, "bf16", 0, seed=18, layout=layout, kind="unif")
+
+
+@pytest.mark.parametrize("layer", ["dw2", "dw4", "dw6", "dw10", "dw14", "dw24", "dw26"])
+def test_candidates_fullsize_b128_fp32_uniform(layer):
+    L = [l for l in synth.mobilenet_v1_dw(128) if l.name == layer][0]
+    _check_layer(L, "f32", 0, seed=19, kind="unif")
+
+
+# configs[3] stress shapes at the bench size (N=64): m = 2/4, K = 5/7 on 56x56x128; stride 2 on 56x56x512
+CFG4 = [synth.Layer("m2", 64, 128, 56, 56, k=3, s=1, p=1, m=2), synth.Layer("m4", 64, 128, 56, 56, k=3, s=1, p=1, m=4),
+        synth.Layer("k5", 64, 128, 56, 56, k=5, s=1, p=2, m=1), synth.Layer("k7", 64, 128, 56, 56, k=7, s=1, p=3, m=1),
+        synth.Layer("s2k3", 64, 512, 56, 56, k=3, s=2, p=1, m=1),
+        synth.Layer("s2k5", 64, 512, 56, 56, k=5, s=2, p=2, m=1),
+        synth.Layer("s2k7", 64, 512, 56, 56, k=7, s=2, p=3, m=1)]
+
+
+@pytest.mark.parametrize("kind", ["int", "unif"])
+@pytest.mark.parametrize("layout", [NCHW, NHWC])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", [L.name for L in CFG4])
+def test_cfg4_fullsize(shape, dtype, layout, kind):
+    L = [l for l in CFG4 if l.name == shape][0]
+    # integer sets of SURVEY c.6: {-1,0,1} keeps bf16 m*K^2 <= 196 <= 256 and every sum < 2^24
+    _check_layer(L, dtype, 1, seed=21, layout=layout, kind=kind)
 
 
 def test_tune_layer_selects_a_candidate():

@@ -224,6 +224,37 @@ def test_mobilenet_layers_random_fp32(_lib):
         check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=NCHW, dtype="f32", kind="unif")
 
 
+# configs[2]: MobileNet-v1 width multipliers x resolutions (Table V).
+# Plane sizes 4..112 and channel counts 8..768 hit planner branches the alpha 1.0 / 224 stack never does.
+CFG3 = [(a, r) for a in (0.25, 0.5, 0.75) for r in (128, 160, 192, 224)]
+
+
+@pytest.mark.parametrize("kind", ["int", "unif"])
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("alpha,res", CFG3)
+def test_cfg3_width_resolution_stack(alpha, res, layout, dtype, kind, _lib):
+    """All 13 depthwise layers of every alpha x R variant at batch 2, both layouts, both dtypes: every
+    output element against the oracle (bitwise on {-2..2} integers, R2/R3 on U[-1,1])."""
+    import synth
+    for L in synth.mobilenet_v1_dw(2, alpha=alpha, resolution=res):
+        check_all(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout=layout, dtype=dtype, kind=kind, amax=2, seed=3)
+
+
+# configs[3] stress shapes at batch 2 (every element; the bench-size versions sample, test_gpu_fullsize.py)
+CFG4_N2 = [(2, 128, 56, 56, 2, 3, 1, 1), (2, 128, 56, 56, 4, 3, 1, 1), (2, 128, 56, 56, 1, 5, 1, 2),
+           (2, 128, 56, 56, 1, 7, 1, 3), (2, 512, 56, 56, 1, 3, 2, 1), (2, 512, 56, 56, 1, 5, 2, 2),
+           (2, 512, 56, 56, 1, 7, 2, 3)]
+
+
+@pytest.mark.parametrize("kind", ["int", "unif"])
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("shape", CFG4_N2)
+def test_cfg4_stress_shapes(shape, layout, dtype, kind, _lib):
+    check_all(*shape, layout=layout, dtype=dtype, kind=kind, amax=1, seed=4)
+
+
 # NHWC fast path (nhwc.cu): m = 1, 3x3, pad 1, C % 4 == 0 -- ragged tiles, several
 # channel-vector counts (grid-stride weight reuse, CV not dividing 256), s = 1, 2.
 NHWC_FAST = [

@@ -358,3 +358,24 @@ def test_round_bf16_single_rounding():
     v = synth.uniform(9, (4096,)).astype(np.float64) * 7.0
     via_f32 = synth._bf16_round_f32(v.astype(np.float32)).astype(np.float64)
     assert np.array_equal(oracle.round_to(v, "bf16"), via_f32)
+
+
+@pytest.mark.parametrize("layout", [NCHW, NHWC])
+@pytest.mark.parametrize("spec", SPECS)
+def test_threaded_oracle_bitwise_equals_sequential(spec, layout):
+    """The all-cores CPU baseline splits only the outer loops over OpenMP threads: every
+    output element (value and sum|terms|) must be bitwise equal to the sequential oracle's."""
+    N, C, H, W, m, K, s, p = spec
+    x, w, dy = (_to_layout(a, layout) if a.ndim == 4 else a for a in _data(spec, _unif))
+    shp = x.shape  # physical shape in the layout (the oracle's convention)
+    runs = []
+    for t in (1, 4):
+        oracle.set_threads(t)
+        try:
+            runs.append([oracle.fwd(x, w, s, p, layout=layout), oracle.bwd_data(dy, w, shp, s, p, layout=layout),
+                         oracle.bwd_filter(x, dy, w.shape, s, p, layout=layout)])
+        finally:
+            oracle.set_threads(1)
+    for r1, r4 in zip(*runs):
+        for a, b in zip(r1, r4):
+            assert np.array_equal(a, b)

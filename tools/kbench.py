@@ -4,7 +4,8 @@ of (layer, pass), plus the same harness around torch's copy_ of the same byte
 count (the practical floor for a kernel that reads |in| and writes |out| bytes).
 
     python tools/kbench.py --layers dw14,dw26 --passes fwd,bwd_filter [--copy]
-Planner env knobs (DWCONV_FD_FORCE, DWCONV_BF_FORCE, ...) apply per process.
+Planner env knobs (DWCONV_FD_FORCE, DWCONV_BF_FORCE, ...) apply per process, in a library built with
+-DDWCONV_DEV_KNOBS only (the shipped build ignores the environment).
 """
 import argparse
 import os
