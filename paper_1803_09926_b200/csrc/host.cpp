@@ -101,6 +101,7 @@ struct Plan {
   ChunkPlan chunk{};
   NhwcPlan nhwc{};
   dwk::NhwcTmaPlan tma{};
+  dwk::BdmmaPlan bdmma{};
 };
 
 // Choose the kernel family for a pass.  Pure host computation, memoised per
@@ -243,6 +244,8 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
     return cuda_status(dwk::launch_nchw_fwd(g, p.chunk, x, w, y, st));
   if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(x, y))
     return cuda_status(dwk::launch_nhwc_tma(g, p.tma, x, w, y, st));
+  if (p.variant == DWCONV_VARIANT_NHWC_BDMMA && tma_aligned(x, y))
+    return cuda_status(dwk::launch_nhwc_bdmma(g, p.bdmma, x, w, y, st));
   if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
       nhwc_aligned(g, x, y))
     return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_FWD, x, w, y, st));
@@ -269,6 +272,8 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
     return cuda_status(dwk::launch_nchw_bwd_data(g, p.chunk, dy, w, dx, st));
   if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(dy, dx))
     return cuda_status(dwk::launch_nhwc_tma(g, p.tma, dy, w, dx, st));
+  if (p.variant == DWCONV_VARIANT_NHWC_BDMMA && tma_aligned(dy, dx))
+    return cuda_status(dwk::launch_nhwc_bdmma(g, p.bdmma, dy, w, dx, st));
   if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
       nhwc_aligned(g, dy, dx))
     return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_BWD_DATA, dy, w, dx, st));
@@ -394,6 +399,11 @@ static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* 
       info->batch_slices = c.nslices; info->max_chain = c.max_chain;
       info->workspace_bytes = (int64_t)std::max(c.ws_bytes, p.nhwc.grid > 0 ? p.nhwc.ws_bytes : (size_t)0);
     }
+  } else if (p.variant == DWCONV_VARIANT_NHWC_BDMMA) {
+    const dwk::BdmmaPlan& c = p.bdmma;
+    info->grid = c.grid; info->block = 192; info->smem_bytes = c.smem; info->launches = 1;
+    info->work_units = (int64_t)c.ncb * c.tiles_per_cb; info->rows_per_band = 8;
+    info->planes_per_chunk = c.S;  // group size S of the block-diagonal weight
   } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
     const NhwcPlan& c = p.nhwc;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
@@ -461,6 +471,18 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
   if (all.empty() && g.layout == DWCONV_NHWC) {
     Plan dp;
     make_plan_uncached(g, pass, di, &dp);
+    // the paper's block-diagonal tensor-core GEMM, group sizes S = 16 / 32 / 64 (where the
+    // diagonal weight tiles fit in shared memory): measured candidates, never the default
+    std::vector<Plan> mma;
+    for (int S : {16, 32, 64}) {
+      Plan v;
+      v.variant = DWCONV_VARIANT_NHWC_BDMMA;
+      if (dwk::plan_nhwc_bdmma(g, pass, di.sms, di.smem_optin, S, &v.bdmma)) mma.push_back(v);
+    }
+    if (dp.variant == DWCONV_VARIANT_GENERIC && !mma.empty()) {
+      all.push_back(dp);
+      all.insert(all.end(), mma.begin(), mma.end());
+    }
     if (dp.variant == DWCONV_VARIANT_NHWC_TMA || dp.variant == DWCONV_VARIANT_NHWC_TILE) {
       all.push_back(dp);
       nhwc_candidates(g, pass, di, &all);
@@ -471,6 +493,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
           all.erase(all.begin() + (long)i);
           break;
         }
+      all.insert(all.end(), mma.begin(), mma.end());
     }
     if ((int)all.size() > DWCONV_MAX_CANDIDATES) all.resize(DWCONV_MAX_CANDIDATES);
     std::lock_guard<std::mutex> lk(g_sel_mu);

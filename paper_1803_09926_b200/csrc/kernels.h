@@ -157,4 +157,14 @@ bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p
 cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* x, const void* dy, float* dw,
                                void* ws, cudaStream_t st);
 
+// ---- the paper's block-diagonal GEMM on tcgen05 (NHWC bf16, m = 1, stride 1, K in {3,5,7}): nhwc_bdmma.cu
+struct BdmmaPlan {
+  int K, S, pass, pad, TW;
+  int tiles_h, tiles_w, tiles_per_cb, ncb, ctas_per_cb;
+  int grid, smem;
+};
+bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S, BdmmaPlan* plan);
+cudaError_t launch_nhwc_bdmma(const Geom& g, const BdmmaPlan& p, const void* in, const void* w, void* out,
+                              cudaStream_t st);
+
 }  // namespace dwk

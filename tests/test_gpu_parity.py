@@ -362,3 +362,50 @@ def test_fused_backward_fallback_and_layers(_lib):
         _, (rdx, adx), (rdw, adw) = run_oracle(inp, L.s, L.p)
         check_close(to_np(dx), rdx, adx, "f32", "fused dx", True)
         check_close(to_np(dwv), rdw, adw, "f32", "fused dw", True)
+
+
+# the paper's block-diagonal GEMM on tcgen05 (NHWC bf16, stride 1, K = 3/5/7, C % 64 == 0),
+# every group size S the library offers, fwd and bwd_data, against the oracle on every element.
+BDMMA_SHAPES = [
+    (2, 64, 16, 16, 1, 3, 1, 1),     # one tile column, ragged rows
+    (2, 128, 37, 45, 1, 3, 1, 1),    # ragged tiles both ways, two channel blocks
+    (1, 64, 28, 28, 1, 5, 1, 2),
+    (2, 128, 23, 61, 1, 7, 1, 3),    # three tile columns (TW = 26), ragged
+    (1, 64, 9, 9, 1, 7, 1, 2),       # padding below (K-1)/2
+    (3, 192, 14, 14, 1, 5, 1, 2),
+]
+
+
+@pytest.mark.parametrize("kind", ["int", "unif"])
+@pytest.mark.parametrize("shape", BDMMA_SHAPES)
+def test_bdmma_candidates(shape, kind, _lib):
+    from paper_1803_09926_b200 import ops
+    from paper_1803_09926_b200._lib import BF16
+    N, C, H, W, m, K, s, p = shape
+    inp = make_inputs(N, C, H, W, m, K, s, p, kind=kind, dtype="bf16", amax=1, seed=5)
+    (y, ay), (dx, adx), _ = run_oracle(inp, s, p)
+    d = ops.make_desc(N, C, H, W, m, K, s, p, NHWC, BF16)
+    x = to_dev(inp["x"], NHWC, "bf16")
+    w = to_dev(inp["w"], NHWC, "bf16")
+    dy = to_dev(inp["dy"], NHWC, "bf16")
+    seen = 0
+    for pas, out, ref, ab in ((0, torch.empty_like(dy), y, ay), (1, torch.empty_like(x), dx, adx)):
+        cands = ops.dwconv_plan_candidates(d, pas)
+        idx = [i for i, c in enumerate(cands) if c["variant_name"] == "nhwc_bdmma"]
+        assert idx, f"no block-diagonal MMA candidate for {shape} pass {pas}"
+        try:
+            for i in idx:
+                ops.dwconv_plan_select(d, pas, i)
+                out.fill_(float("nan"))
+                if pas == 0:
+                    ops.dwconv_fwd(d, x, w, out)
+                else:
+                    ops.dwconv_bwd_data(d, dy, w, out)
+                torch.cuda.synchronize()
+                got = out.float().contiguous().cpu().numpy().astype(np.float64)
+                check_close(got, ref, ab, "bf16", f"bdmma S={cands[i]['planes_per_chunk']} pass {pas}",
+                            kind == "int")
+                seen += 1
+        finally:
+            ops.dwconv_plan_select(d, pas, -1)
+    assert seen >= 2
