@@ -158,8 +158,9 @@ typedef enum {
   DWCONV_VARIANT_NHWC_TILE = 3,   /* NHWC: spatial x channel-vector register tiles, L1 loads */
   DWCONV_VARIANT_NHWC_TMA = 4,    /* NHWC: 4-D tensor-map TMA boxes with zero-filled halos  */
   DWCONV_VARIANT_NHWC_BDMMA = 5   /* NHWC bf16: the paper's block-diagonal GEMM on tcgen05 tensor
-                                     cores (Eqs. 1-3), group size S in planes_per_chunk;
-                                     a measured candidate only, never the default */
+                                     cores (Eqs. 1-3); group size S in planes_per_chunk,
+                                     staged channel block in rows_per_band; a measured candidate
+                                     only, never the default */
 } dwconv_variant;
 typedef struct {
   int32_t variant;            /* dwconv_variant */

@@ -402,8 +402,9 @@ static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* 
   } else if (p.variant == DWCONV_VARIANT_NHWC_BDMMA) {
     const dwk::BdmmaPlan& c = p.bdmma;
     info->grid = c.grid; info->block = 192; info->smem_bytes = c.smem; info->launches = 1;
-    info->work_units = (int64_t)c.ncb * c.tiles_per_cb; info->rows_per_band = 8;
-    info->planes_per_chunk = c.S;  // group size S of the block-diagonal weight
+    info->work_units = (int64_t)c.ncb * c.tiles_per_cb;
+    info->planes_per_chunk = c.S;   // group size S of the block-diagonal weight
+    info->rows_per_band = c.CB;     // staged channel block (A rows of CB*2 bytes)
   } else if (p.variant == DWCONV_VARIANT_NHWC_TILE) {
     const NhwcPlan& c = p.nhwc;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
@@ -471,13 +472,15 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
   if (all.empty() && g.layout == DWCONV_NHWC) {
     Plan dp;
     make_plan_uncached(g, pass, di, &dp);
-    // the paper's block-diagonal tensor-core GEMM, group sizes S = 16 / 32 / 64 (where the
-    // diagonal weight tiles fit in shared memory): measured candidates, never the default
+    // the paper's block-diagonal tensor-core GEMM, group sizes S = 16 / 32 / 64 over channel
+    // blocks CB >= S (where the diagonal weight tiles fit in shared memory): measured
+    // candidates, never the default
     std::vector<Plan> mma;
-    for (int S : {16, 32, 64}) {
+    static const int sc[][2] = {{16, 16}, {16, 32}, {32, 32}, {16, 64}, {32, 64}, {64, 64}};  // {S, CB}
+    for (const auto& q : sc) {
       Plan v;
       v.variant = DWCONV_VARIANT_NHWC_BDMMA;
-      if (dwk::plan_nhwc_bdmma(g, pass, di.sms, di.smem_optin, S, &v.bdmma)) mma.push_back(v);
+      if (dwk::plan_nhwc_bdmma(g, pass, di.sms, di.smem_optin, q[0], q[1], &v.bdmma)) mma.push_back(v);
     }
     if (dp.variant == DWCONV_VARIANT_GENERIC && !mma.empty()) {
       all.push_back(dp);

@@ -159,11 +159,11 @@ cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* 
 
 // ---- the paper's block-diagonal GEMM on tcgen05 (NHWC bf16, m = 1, stride 1, K in {3,5,7}): nhwc_bdmma.cu
 struct BdmmaPlan {
-  int K, S, pass, pad, TW;
+  int K, S, CB, pass, pad, TW;
   int tiles_h, tiles_w, tiles_per_cb, ncb, ctas_per_cb;
   int grid, smem;
 };
-bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S, BdmmaPlan* plan);
+bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S, int CB, BdmmaPlan* plan);
 cudaError_t launch_nhwc_bdmma(const Geom& g, const BdmmaPlan& p, const void* in, const void* w, void* out,
                               cudaStream_t st);
 

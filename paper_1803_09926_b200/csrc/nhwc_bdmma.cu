@@ -51,13 +51,20 @@ namespace dwk {
 namespace bdmma {
 
 constexpr int BW = 32;                 // staged box width in pixels = flat row pitch of the implicit GEMM
-constexpr int TH = 8;                  // output rows per tile
-constexpr int CB = 64;                 // channels per tile: one 128-B SWIZZLE_128B row per pixel
-constexpr int MT = TH * BW / 128;      // M tiles (128 flat positions) per staged tile
-constexpr int NACC = 4;                // TMEM accumulators of 64 fp32 columns
 constexpr int NS = 2;                  // input ring stages
-constexpr int kThreads = 192;
-constexpr uint32_t kTmemCols = NACC * CB;
+constexpr int kThreads = 224;            // producer, 2 MMA issuers, 4 epilogue warps
+constexpr uint32_t kTmemCols = 256;    // accumulators: 2 stages x MT tiles x CB fp32 columns
+// Channel block CB (16 / 32 / 64 bf16 = one 32 / 64 / 128-B swizzled row per pixel): the TMA
+// box, the tensor core's A rows and the accumulator width.  TH output rows per tile keep a
+// stage's box near the same size: TH * CB = 512, MT = TH * BW / 128 M tiles per tile.
+template <int CB> struct Blk {
+  static constexpr int TH = 512 / CB;
+  static constexpr int MT = TH * BW / 128;
+  static constexpr int NACC = 2 * MT;
+  static constexpr int ROWB = CB * 2;                          // bytes per staged pixel
+  static constexpr uint32_t LAYOUT = CB == 64 ? 2 : (CB == 32 ? 4 : 6);  // UMMA SWIZZLE_128B / 64B / 32B
+  static_assert(NACC * CB == (int)kTmemCols, "TMEM budget");
+};
 
 struct Args {
   __nv_bfloat16* out;
@@ -67,8 +74,8 @@ struct Args {
   int tiles_h, tiles_w;    // tiles per image
   int tiles_per_cb;        // N * tiles_h * tiles_w
   int ctas_per_cb;
-  uint32_t stage_bytes;    // (BH + 1) * BW * 128 (one spare row: ragged flat columns read past the box)
-  uint32_t box_bytes;      // BH * BW * 128
+  uint32_t stage_bytes;    // (BH + 1) * BW * ROWB (one spare row: ragged flat columns read past the box)
+  uint32_t box_bytes;      // BH * BW * ROWB
   uint32_t bw_bytes;       // diagonal weight tiles
   int flip;                // bwd_data: kernel rotated 180 degrees
 };
@@ -112,15 +119,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// 32 TMEM columns of this warp's 32 lanes -> 32 registers per thread.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+// 16 TMEM columns of this warp's 32 lanes -> 16 registers per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -130,13 +134,14 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int K, int S>
+template <int K, int S, int CB>
 __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constant__ CUtensorMap tm, const Args a) {
-  constexpr int G = CB / S;      // groups per 64-channel block
+  constexpr int G = CB / S;      // groups per channel block
   constexpr int KC = S / 16;     // 16-channel K chunks per group
+  constexpr int TH = Blk<CB>::TH, MT = Blk<CB>::MT, NACC = Blk<CB>::NACC, ROWB = Blk<CB>::ROWB;
   constexpr uint32_t kIdesc = instr_desc(128, S);
   extern __shared__ unsigned char smem_raw[];
-  // 1024-B alignment for the SWIZZLE_128B stages (the host adds 1 KB of slack)
+  // 1024-B alignment for the swizzled stages (the host adds 1 KB of slack)
   unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* stages = smem;
   unsigned char* bw = smem + NS * a.stage_bytes;
@@ -206,44 +211,56 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
                     &full[s]);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 1 || warp == 2) {
+    // ------------------------------------------------------------ MMA issuers
+    // Warp 1 issues the MMAs of the tiles in ring stage 0, warp 2 those of stage 1: the
+    // tensor core runs the two instruction streams concurrently, while MMAs of one stream
+    // execute one after another (measured: one stream keeps the tensor core's shared-memory
+    // operand reads at ~1/3 of the SMEM bandwidth, ~110 clk per M=128 K=16 MMA).
     if (lane == 0) {
-      int it = 0, acc_it = 0;
-      const uint32_t st0 = smem_u32(stages), bw0 = smem_u32(bw);
-      for (int t = local; t < a.tiles_per_cb; t += a.ctas_per_cb, ++it) {
-        const int s = it % NS;
+      const int s = warp - 1;
+      const uint32_t st0 = smem_u32(stages), bw0 = smem_u32(bw);  // < 2^18: start field never carries
+      const uint32_t sa = st0 + (uint32_t)s * a.stage_bytes;
+      const uint64_t abase = smem_desc(sa, 16, 8 * ROWB, Blk<CB>::LAYOUT, 0);
+      const uint64_t bbase = smem_desc(bw0, 128, 256, 0, 0);
+      int it = s;
+      for (int t = local + s * a.ctas_per_cb; t < a.tiles_per_cb; t += NS * a.ctas_per_cb, it += NS) {
         mbar_wait(&full[s], (it / NS) & 1);
+        // this stage's MT accumulators: wait until the epilogue has drained each
+        if (it >= NS)
+          for (int mt = 0; mt < MT; ++mt) mbar_wait(&tempty[s * MT + mt], ((it / NS) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t sa = st0 + (uint32_t)s * a.stage_bytes;
-        for (int mt = 0; mt < MT; ++mt, ++acc_it) {
-          const int ac = acc_it % NACC;
-          if (acc_it >= NACC) mbar_wait(&tempty[ac], ((acc_it / NACC) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t d0 = tbase + (uint32_t)(ac * CB);
+        // taps outer, M tiles inner: consecutive MMAs accumulate into different TMEM
+        // accumulators (independent chains); descriptors advance by adding to the
+        // start-address field (16-B units) of a base descriptor
 #pragma unroll 1
-          for (int tap = 0; tap < K * K; ++tap) {
-            const int i = tap / K, j = tap - i * K;
-            const uint32_t rowa = sa + (uint32_t)((mt * 128 + i * BW + j) * 128);
+        for (int tap = 0; tap < K * K; ++tap) {
+          const int i = tap / K, j = tap - i * K;
+          const uint32_t arow = (uint32_t)((i * BW + j) * ROWB);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint32_t d0 = tbase + (uint32_t)((s * MT + mt) * CB);
 #pragma unroll
             for (int g = 0; g < G; ++g) {
 #pragma unroll
               for (int kc = 0; kc < KC; ++kc) {
-                const uint32_t aaddr = rowa + (uint32_t)((g * S + kc * 16) * 2);
-                const uint64_t ad = smem_desc(aaddr, 16, 1024, 2, (aaddr >> 7) & 7);
-                const uint64_t bd = smem_desc(bw0 + (uint32_t)(((tap * G + g) * KC + kc) * S * 32), 128, 256, 0, 0);
+                // base offset 0 at ANY row shift: the swizzle XOR is taken from the absolute
+                // shared-memory address, like the TMA write (tools/umma_probe.cu: every shift 0..127
+                // exact with 0, wrong with (addr >> 7) & 7)
+                const uint64_t ad = abase + ((arow + (uint32_t)(mt * 128 * ROWB + (g * S + kc * 16) * 2)) >> 4);
+                const uint64_t bd = bbase + ((uint32_t)(((tap * G + g) * KC + kc) * S * 32) >> 4);
                 mma_bf16(d0 + (uint32_t)(g * S), ad, bd, kIdesc, (tap | kc) != 0);
               }
             }
           }
-          mma_commit(&tfull[ac]);
         }
+        for (int mt = 0; mt < MT; ++mt) mma_commit(&tfull[s * MT + mt]);
         mma_commit(&empty[s]);  // the stage is free once every MMA reading it has completed
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;  // TMEM lane quarter this warp may access (warps 3-6 cover all four)
     int acc_it = 0;
     for (int t = local; t < a.tiles_per_cb; t += a.ctas_per_cb) {
       const int n = t / per_img, r0 = t - n * per_img;
@@ -256,9 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
         const int row = mt * 128 + q * 32 + lane;
         const int r = row / BW, c = row - r * BW;
         const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(ac * CB);
-        uint32_t v0[32], v1[32];
-        tmem_ld32(ta, v0);
-        tmem_ld32(ta + 32, v1);
+        uint32_t v[CB];
+#pragma unroll
+        for (int u = 0; u < CB / 16; ++u) tmem_ld16(ta + 16 * u, &v[16 * u]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -267,13 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
         if (c < a.TW && oh < a.OH && ow < a.OW) {
           uint4* dst = reinterpret_cast<uint4*>(a.out + (((size_t)n * a.OH + oh) * a.OW + ow) * a.C + cb * CB);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            dst[u] = make_uint4(pack_bf16(v0[8 * u], v0[8 * u + 1]), pack_bf16(v0[8 * u + 2], v0[8 * u + 3]),
-                                pack_bf16(v0[8 * u + 4], v0[8 * u + 5]), pack_bf16(v0[8 * u + 6], v0[8 * u + 7]));
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            dst[4 + u] = make_uint4(pack_bf16(v1[8 * u], v1[8 * u + 1]), pack_bf16(v1[8 * u + 2], v1[8 * u + 3]),
-                                    pack_bf16(v1[8 * u + 4], v1[8 * u + 5]), pack_bf16(v1[8 * u + 6], v1[8 * u + 7]));
+          for (int u = 0; u < CB / 8; ++u)
+            dst[u] = make_uint4(pack_bf16(v[8 * u], v[8 * u + 1]), pack_bf16(v[8 * u + 2], v[8 * u + 3]),
+                                pack_bf16(v[8 * u + 4], v[8 * u + 5]), pack_bf16(v[8 * u + 6], v[8 * u + 7]));
         }
       }
     }
@@ -289,20 +302,23 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
 
 using KernelFn = void (*)(const CUtensorMap, const Args);
 
+// group size S (the block-diagonal weight's width) needs a channel block CB >= S; CB = 16 / 32
+// also staged for S = 16 (the swizzled A rows the tensor core reads per MMA are CB*2 bytes)
 template <int K>
-KernelFn pick_s(int S) {
-  if (S == 16) return bdmma_kernel<K, 16>;
-  if constexpr (K <= 5)
-    if (S == 32) return bdmma_kernel<K, 32>;
-  if constexpr (K == 3)
-    if (S == 64) return bdmma_kernel<K, 64>;
+KernelFn pick(int S, int CB) {
+  if (S == 16 && CB == 16) return bdmma_kernel<K, 16, 16>;
+  if (S == 16 && CB == 32) return bdmma_kernel<K, 16, 32>;
+  if (S == 32 && CB == 32) return bdmma_kernel<K, 32, 32>;
+  if (S == 16 && CB == 64) return bdmma_kernel<K, 16, 64>;
+  if (S == 32 && CB == 64) return bdmma_kernel<K, 32, 64>;
+  if (S == 64 && CB == 64) return bdmma_kernel<K, 64, 64>;
   return nullptr;
 }
-KernelFn kernel_for(int K, int S) {
+KernelFn kernel_for(int K, int S, int CB) {
   switch (K) {
-    case 3: return pick_s<3>(S);
-    case 5: return pick_s<5>(S);
-    case 7: return pick_s<7>(S);
+    case 3: return pick<3>(S, CB);
+    case 5: return pick<5>(S, CB);
+    case 7: return pick<7>(S, CB);
     default: return nullptr;
   }
 }
@@ -334,29 +350,34 @@ bool opt_in_smem(const void* fn, int bytes) {
   return true;
 }
 
-int smem_bytes(int K, int S) {
-  const int BH = TH + K - 1;
-  return 1024 + NS * (BH + 1) * BW * 128 + K * K * 128 * S + (2 * NS + 2 * NACC) * 8 + 16;
+int th_of(int CB) { return 512 / CB; }
+
+int smem_bytes(int K, int S, int CB) {
+  const int BH = th_of(CB) + K - 1;
+  const int nacc = 2 * (th_of(CB) * BW / 128);
+  return 1024 + NS * (BH + 1) * BW * CB * 2 + K * K * (CB / S) * S * S * 2 + (2 * NS + 2 * nacc) * 8 + 16;
 }
 
 }  // namespace bdmma
 
-bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S, BdmmaPlan* p) {
+bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S, int CB, BdmmaPlan* p) {
   using namespace bdmma;
   if (g.layout != DWCONV_NHWC || g.dtype != DWCONV_BF16 || g.m != 1 || g.kh != g.kw || g.sh != 1 || g.sw != 1 ||
       g.ph != g.pw || (pass != DWCONV_PASS_FWD && pass != DWCONV_PASS_BWD_DATA))
     return false;
   const int K = g.kh;
   if (K != 3 && K != 5 && K != 7) return false;
-  if (g.C % CB != 0 || !kernel_for(K, S)) return false;
+  KernelFn fn = kernel_for(K, S, CB);
+  if (!fn || g.C % CB != 0) return false;
   const int pad = pass == DWCONV_PASS_FWD ? g.ph : K - 1 - g.ph;
   if (pad < 0 || pad > K - 1) return false;
-  const int smem = smem_bytes(K, S);
+  const int smem = smem_bytes(K, S, CB);
   if (smem > smem_optin) return false;
   const int64_t OH = pass == DWCONV_PASS_FWD ? g.Ho : g.H, OW = pass == DWCONV_PASS_FWD ? g.Wo : g.W;
-  const int TW = BW - K + 1;
+  const int TW = BW - K + 1, TH = th_of(CB);
   p->K = K;
   p->S = S;
+  p->CB = CB;
   p->pass = pass;
   p->TW = TW;
   p->tiles_h = (int)((OH + TH - 1) / TH);
@@ -365,8 +386,14 @@ bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S
   if (per_cb >= (1ll << 30)) return false;
   p->tiles_per_cb = (int)per_cb;
   p->ncb = (int)(g.C / CB);
-  // about one CTA per SM (1 CTA/SM: ~100-220 KB of shared memory), every CTA on one channel block
-  p->ctas_per_cb = (int)std::max<int64_t>(1, std::min<int64_t>(per_cb, (num_sms + p->ncb - 1) / p->ncb));
+  // one wave: resident CTAs per SM (shared memory; TMEM: 256 columns each, so at most 2) x SMs,
+  // every CTA on one channel block (its diagonal weight tiles are built once)
+  if (!opt_in_smem(reinterpret_cast<const void*>(fn), smem)) return false;
+  int dev = 0, sm_smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const int occ = std::max(1, std::min(2, sm_smem / (smem + 1024)));  // TMEM: 256 columns each
+  p->ctas_per_cb = (int)std::max<int64_t>(1, std::min<int64_t>(per_cb, (occ * num_sms) / p->ncb));
   p->grid = p->ncb * p->ctas_per_cb;
   p->smem = smem;
   p->pad = pad;
@@ -376,19 +403,21 @@ bool plan_nhwc_bdmma(const Geom& g, int pass, int num_sms, int smem_optin, int S
 cudaError_t launch_nhwc_bdmma(const Geom& g, const BdmmaPlan& p, const void* in, const void* w, void* out,
                               cudaStream_t st) {
   using namespace bdmma;
-  KernelFn fn = kernel_for(p.K, p.S);
+  KernelFn fn = kernel_for(p.K, p.S, p.CB);
   EncodeFn enc = encode_fn();
   if (!fn || !enc) return cudaErrorNotSupported;
   const bool fwd = p.pass == DWCONV_PASS_FWD;
   const int64_t IH = fwd ? g.H : g.Ho, IW = fwd ? g.W : g.Wo;
-  const int BH = TH + p.K - 1;
+  const int BH = th_of(p.CB) + p.K - 1, ROWB = p.CB * 2;
   CUtensorMap tm;
   const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)IW, (cuuint64_t)IH, (cuuint64_t)g.N};
   const cuuint64_t strides[3] = {(cuuint64_t)g.C * 2, (cuuint64_t)(IW * g.C * 2), (cuuint64_t)(IH * IW * g.C * 2)};
-  const cuuint32_t box[4] = {(cuuint32_t)CB, (cuuint32_t)BW, (cuuint32_t)BH, 1};
+  const cuuint32_t box[4] = {(cuuint32_t)p.CB, (cuuint32_t)BW, (cuuint32_t)BH, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle sw = p.CB == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                           : (p.CB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(in), dims, strides, box, es,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   Args a{};
@@ -404,9 +433,9 @@ cudaError_t launch_nhwc_bdmma(const Geom& g, const BdmmaPlan& p, const void* in,
   a.tiles_w = p.tiles_w;
   a.tiles_per_cb = p.tiles_per_cb;
   a.ctas_per_cb = p.ctas_per_cb;
-  a.stage_bytes = (uint32_t)((BH + 1) * BW * 128);
-  a.box_bytes = (uint32_t)(BH * BW * 128);
-  a.bw_bytes = (uint32_t)(p.K * p.K * 128 * p.S);
+  a.stage_bytes = (uint32_t)((BH + 1) * BW * ROWB);
+  a.box_bytes = (uint32_t)(BH * BW * ROWB);
+  a.bw_bytes = (uint32_t)(p.K * p.K * p.CB * p.S * 2);
   a.flip = fwd ? 0 : 1;
   if (!opt_in_smem(reinterpret_cast<const void*>(fn), p.smem)) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg{};

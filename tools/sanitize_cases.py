@@ -30,6 +30,7 @@ CASES = [  # name, (N, C, H, W, m, K, s, p), layout, dtype
     ("k5", (2, 32, 28, 28, 1, 5, 1, 2), NCHW, "f32"),
     ("k7_nhwc", (2, 32, 28, 28, 1, 7, 1, 3), NHWC, "bf16"),
     ("m2", (2, 16, 28, 28, 2, 3, 1, 1), NHWC, "f32"),
+    ("bdmma_k5", (2, 64, 20, 20, 1, 5, 1, 2), NHWC, "bf16"),  # tcgen05 block-diagonal candidates
 ]
 
 

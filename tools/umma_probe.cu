@@ -142,8 +142,8 @@ int main() {
   int bad = 0;
   for (int base = 0; base < 2; ++base)
     for (int s : {0, 1, 3, 8, 13, 40, 127}) bad += run<16>(s, base) ? 1 : 0;
-  for (int s : {0, 5, 33}) bad += run<32>(s, 1) ? 1 : 0;
-  for (int s : {0, 7, 66}) bad += run<64>(s, 1) ? 1 : 0;
+  for (int s : {0, 5, 33}) bad += run<32>(s, 0) ? 1 : 0;
+  for (int s : {0, 7, 66}) bad += run<64>(s, 0) ? 1 : 0;
   printf("probe done, %d failing configs\n", bad);
   return 0;
 }
