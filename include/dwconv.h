@@ -157,10 +157,12 @@ typedef enum {
   DWCONV_VARIANT_NCHW_CHUNK = 2,  /* NCHW: whole planes / row bands staged by bulk TMA      */
   DWCONV_VARIANT_NHWC_TILE = 3,   /* NHWC: spatial x channel-vector register tiles, L1 loads */
   DWCONV_VARIANT_NHWC_TMA = 4,    /* NHWC: 4-D tensor-map TMA boxes with zero-filled halos  */
-  DWCONV_VARIANT_NHWC_BDMMA = 5   /* NHWC bf16: the paper's block-diagonal GEMM on tcgen05 tensor
+  DWCONV_VARIANT_NHWC_BDMMA = 5,  /* NHWC bf16: the paper's block-diagonal GEMM on tcgen05 tensor
                                      cores (Eqs. 1-3); group size S in planes_per_chunk,
                                      staged channel block in rows_per_band; a measured candidate
                                      only, never the default */
+  DWCONV_VARIANT_NHWC_GEN = 6     /* NHWC: K x K (3/5/7) stride 1/2 multiplier 1/2/4 register
+                                     tiles, weights staged in shared memory */
 } dwconv_variant;
 typedef struct {
   int32_t variant;            /* dwconv_variant */

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libdwconv.so")
 NCHW, NHWC = 0, 1
 F32, BF16 = 0, 1
 PASS_FWD, PASS_BWD_DATA, PASS_BWD_FILTER, PASS_BWD = 0, 1, 2, 3
-VARIANTS = {0: "none", 1: "generic", 2: "nchw_chunk", 3: "nhwc_tile", 4: "nhwc_tma", 5: "nhwc_bdmma"}
+VARIANTS = {0: "none", 1: "generic", 2: "nchw_chunk", 3: "nhwc_tile", 4: "nhwc_tma", 5: "nhwc_bdmma", 6: "nhwc_gen"}
 FUNCTIONS = ("dwconv_abi_version", "dwconv_status_string", "dwconv_output_shape", "dwconv_fwd",
              "dwconv_bwd_data", "dwconv_bwd_filter_workspace_bytes", "dwconv_bwd_filter",
              "dwconv_bwd_workspace_bytes", "dwconv_bwd",

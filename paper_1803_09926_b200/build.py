@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 SOURCES = ["host.cpp", "generic.cu", "nchw_plan.cu", "nchw_fwd.cu", "nchw_bwd_data.cu", "nchw_bwd_filter.cu",
-           "direct_bwd_filter.cu", "nhwc.cu", "nhwc_tma.cu", "nchw_small.cu", "nhwc_bdmma.cu"]
+           "direct_bwd_filter.cu", "nhwc.cu", "nhwc_tma.cu", "nchw_small.cu", "nhwc_bdmma.cu", "nhwc_gen.cu"]
 HEADERS = ["common.cuh", "kernels.h", "nchw_common.cuh"]
 
 

@@ -102,6 +102,7 @@ struct Plan {
   NhwcPlan nhwc{};
   dwk::NhwcTmaPlan tma{};
   dwk::BdmmaPlan bdmma{};
+  dwk::NhwcGenPlan gen{};
 };
 
 // Choose the kernel family for a pass.  Pure host computation, memoised per
@@ -172,7 +173,14 @@ void make_plan_uncached(const Geom& g, int pass, const DevInfo& di, Plan* p) {
     if (!dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->nhwc = NhwcPlan{};  // for unaligned pointers
     return;
   }
-  if (g.layout == DWCONV_NHWC && dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) p->variant = DWCONV_VARIANT_NHWC_TILE;
+  if (g.layout == DWCONV_NHWC && dwk::plan_nhwc(g, pass, di.sms, &p->nhwc)) {
+    p->variant = DWCONV_VARIANT_NHWC_TILE;
+    return;
+  }
+  // K = 5 / 7, m = 2 / 4, the rest of stride 1 / 2: the general NHWC register-tile kernels
+  if (g.layout == DWCONV_NHWC && dwk::plan_nhwc_gen(g, pass, di.sms, di.smem_optin, &p->gen) &&
+      (pass != DWCONV_PASS_BWD_FILTER || p->gen.max_chain <= 160))
+    p->variant = DWCONV_VARIANT_NHWC_GEN;
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? DWCONV_OK : DWCONV_ERR_CUDA; }
@@ -246,6 +254,8 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
     return cuda_status(dwk::launch_nhwc_tma(g, p.tma, x, w, y, st));
   if (p.variant == DWCONV_VARIANT_NHWC_BDMMA && tma_aligned(x, y))
     return cuda_status(dwk::launch_nhwc_bdmma(g, p.bdmma, x, w, y, st));
+  if (p.variant == DWCONV_VARIANT_NHWC_GEN && tma_aligned(x, y))
+    return cuda_status(dwk::launch_nhwc_gen_fd(g, p.gen, x, w, y, st));
   if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
       nhwc_aligned(g, x, y))
     return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_FWD, x, w, y, st));
@@ -274,6 +284,8 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
     return cuda_status(dwk::launch_nhwc_tma(g, p.tma, dy, w, dx, st));
   if (p.variant == DWCONV_VARIANT_NHWC_BDMMA && tma_aligned(dy, dx))
     return cuda_status(dwk::launch_nhwc_bdmma(g, p.bdmma, dy, w, dx, st));
+  if (p.variant == DWCONV_VARIANT_NHWC_GEN && tma_aligned(dy, dx))
+    return cuda_status(dwk::launch_nhwc_gen_fd(g, p.gen, dy, w, dx, st));
   if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
       nhwc_aligned(g, dy, dx))
     return cuda_status(dwk::launch_nhwc_fd(g, p.nhwc, DWCONV_PASS_BWD_DATA, dy, w, dx, st));
@@ -288,6 +300,7 @@ size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
   Plan p;
   make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
   if (p.variant == DWCONV_VARIANT_NHWC_TILE) return p.nhwc.ws_bytes;
+  if (p.variant == DWCONV_VARIANT_NHWC_GEN) return p.gen.ws_bytes;
   if (p.variant == DWCONV_VARIANT_NHWC_TMA)  // either NHWC kernel may run (pointer alignment)
     return std::max(p.tma.ws_bytes, p.nhwc.grid > 0 ? p.nhwc.ws_bytes : (size_t)0);
   return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? p.chunk.ws_bytes : 0;
@@ -329,6 +342,12 @@ int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float
     if (!workspace) return DWCONV_ERR_NULL_POINTER;
     if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
     return cuda_status(dwk::launch_nhwc_bwd_filter(g, p.nhwc, x, dy, dw, workspace, st));
+  }
+  if (p.variant == DWCONV_VARIANT_NHWC_GEN && tma_aligned(x, dy)) {
+    if (workspace_bytes < p.gen.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
+    if (!workspace) return DWCONV_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
+    return cuda_status(dwk::launch_nhwc_gen_bf(g, p.gen, x, dy, dw, workspace, st));
   }
   return cuda_status(dwk::launch_generic_bwd_filter(g, x, dy, dw, st));
 }
@@ -398,6 +417,15 @@ static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* 
       info->work_units = (int64_t)c.ncb * c.tiles_per_cb;
       info->batch_slices = c.nslices; info->max_chain = c.max_chain;
       info->workspace_bytes = (int64_t)std::max(c.ws_bytes, p.nhwc.grid > 0 ? p.nhwc.ws_bytes : (size_t)0);
+    }
+  } else if (p.variant == DWCONV_VARIANT_NHWC_GEN) {
+    const dwk::NhwcGenPlan& c = p.gen;
+    info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
+    if (pass == DWCONV_PASS_BWD_FILTER) {
+      info->work_units = (int64_t)c.ncb * c.nslices; info->batch_slices = c.nslices;
+      info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+    } else {
+      info->work_units = c.tiles * c.ncb; info->rows_per_band = c.TH; info->planes_per_chunk = c.TW;
     }
   } else if (p.variant == DWCONV_VARIANT_NHWC_BDMMA) {
     const dwk::BdmmaPlan& c = p.bdmma;
@@ -482,7 +510,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
       v.variant = DWCONV_VARIANT_NHWC_BDMMA;
       if (dwk::plan_nhwc_bdmma(g, pass, di.sms, di.smem_optin, q[0], q[1], &v.bdmma)) mma.push_back(v);
     }
-    if (dp.variant == DWCONV_VARIANT_GENERIC && !mma.empty()) {
+    if ((dp.variant == DWCONV_VARIANT_GENERIC || dp.variant == DWCONV_VARIANT_NHWC_GEN) && !mma.empty()) {
       all.push_back(dp);
       all.insert(all.end(), mma.begin(), mma.end());
     }

@@ -157,6 +157,21 @@ bool plan_nhwc_tma_bf(const Geom& g, int num_sms, int smem_optin, NhwcTmaPlan* p
 cudaError_t launch_nhwc_tma_bf(const Geom& g, const NhwcTmaPlan& p, const void* x, const void* dy, float* dw,
                                void* ws, cudaStream_t st);
 
+// ---- NHWC K x K (3/5/7), stride 1/2, multiplier 1/2/4 register-tile kernels: nhwc_gen.cu
+struct NhwcGenPlan {
+  int K, S, M, pass;
+  int CVB, ncb, threads, grid, smem;
+  int TH, TW, OHB, OWB, slots, ctas_per_cb;  // fwd / bwd_data
+  int64_t tiles;
+  int PS, nslices, rps, max_chain;            // bwd_filter
+  size_t part_off, l2_off, t1_off, t2_off, ws_bytes;
+};
+bool plan_nhwc_gen(const Geom& g, int pass, int num_sms, int smem_optin, NhwcGenPlan* plan);
+cudaError_t launch_nhwc_gen_fd(const Geom& g, const NhwcGenPlan& p, const void* in, const void* w, void* out,
+                               cudaStream_t st);
+cudaError_t launch_nhwc_gen_bf(const Geom& g, const NhwcGenPlan& p, const void* x, const void* dy, float* dw,
+                               void* ws, cudaStream_t st);
+
 // ---- the paper's block-diagonal GEMM on tcgen05 (NHWC bf16, m = 1, stride 1, K in {3,5,7}): nhwc_bdmma.cu
 struct BdmmaPlan {
   int K, S, CB, pass, pad, TW;

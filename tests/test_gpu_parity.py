@@ -409,3 +409,31 @@ def test_bdmma_candidates(shape, kind, _lib):
         finally:
             ops.dwconv_plan_select(d, pas, -1)
     assert seen >= 4
+
+
+# NHWC general kernels (nhwc_gen.cu): K = 3/5/7, stride 1/2, m = 1/2/4, C % 4 == 0, pad (K-1)/2 -- the shapes
+# the 3x3 / m = 1 NHWC families do not take.  Ragged tiles, odd sizes, one and several channel blocks.
+NHWC_GEN_SHAPES = [
+    (2, 8, 13, 11, 2, 3, 1, 1),
+    (2, 12, 9, 10, 4, 3, 1, 1),
+    (1, 16, 15, 17, 1, 5, 1, 2),
+    (2, 8, 14, 13, 1, 7, 1, 3),
+    (2, 140, 11, 9, 1, 5, 2, 2),     # 35 channel vectors: two channel blocks, ragged
+    (1, 8, 17, 15, 1, 7, 2, 3),
+    (2, 4, 12, 12, 2, 5, 2, 2),
+    (3, 8, 7, 9, 4, 3, 2, 1),
+    (2, 4, 8, 8, 2, 7, 1, 3),
+]
+
+
+@pytest.mark.parametrize("kind", ["int", "unif"])
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", NHWC_GEN_SHAPES)
+def test_nhwc_gen_kernels(shape, dtype, kind, _lib):
+    from paper_1803_09926_b200 import ops
+    from paper_1803_09926_b200._lib import BF16, F32
+    N, C, H, W, m, K, s, p = shape
+    d = ops.make_desc(N, C, H, W, m, K, s, p, NHWC, F32 if dtype == "f32" else BF16)
+    for pas in (0, 1, 2):
+        assert ops.dwconv_plan(d, pas)["variant_name"] == "nhwc_gen", (shape, pas)
+    check_all(*shape, layout=NHWC, dtype=dtype, kind=kind, amax=1, seed=6)
