@@ -455,9 +455,40 @@ __device__ __forceinline__ void load_row2(const T* row, int c0, float* xv) {  //
 }
 
 // bf16 plane pairs (stride 1): a warp task is 8 planes; lane (p, column group)
-// owns planes p and p + 4 and runs their stencils together with packed FFMA2
-// (lanes of the float2 = the two planes), halving the FMA instructions per
-// output of the bf16 kernels, which are instruction-bound.
+// owns two planes and runs their stencils together with packed FFMA2 (lanes of
+// the float2 = the two planes), halving the FMA instructions per output of the
+// bf16 kernels, which are instruction-bound.
+//
+// Which two planes, and where they sit in shared memory, is chosen against bank
+// conflicts (ncu, W = 14: 74% of the shared-load wavefronts were conflicts with
+// planes p and p + 4 packed back to back -- the four planes one load touches sat
+// 2 banks apart).  W = 7: planes p, p + 4, packed (already conflict-free).
+// W = 14 / 28: ADJACENT planes 2p, 2p + 1 (pair p); W = 14 stages each pair by its
+// own bulk copy at a pitch of 400 elements (200 words = 8 banks, so the four
+// pairs' rows land on disjoint banks: one wavefront per load instead of four);
+// W = 28 keeps one copy (a pair is 784 words = 16 banks apart).
+template <int W> struct PairLayout {
+  static constexpr int HW = W * W;
+  static constexpr bool ADJ = W != 7;                  // planes (2p, 2p+1) instead of (p, p+4)
+  static constexpr int QP = (W == 14) ? 400 : 2 * HW;  // pair pitch in elements (ADJ)
+  static constexpr bool SPLIT = ADJ && QP != 2 * HW;   // one bulk copy per pair
+  static constexpr int REGION = ADJ ? 4 * QP : 8 * HW;  // elements of one 8-plane task in the slot
+  __host__ __device__ static constexpr int plane_a(int p) { return ADJ ? 2 * p : p; }
+  __host__ __device__ static constexpr int plane_b(int p) { return ADJ ? 2 * p + 1 : p + 4; }
+  __host__ __device__ static constexpr int off(int plane) { return ADJ ? (plane >> 1) * QP + (plane & 1) * HW : plane * HW; }
+};
+
+// stage the 8 planes starting at src (contiguous in global) into a slot region
+template <int W>
+__device__ __forceinline__ void stage_pairs(__nv_bfloat16* dst, const __nv_bfloat16* src, uint64_t* bar) {
+  using L = PairLayout<W>;
+  if constexpr (L::SPLIT) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bulk_g2s(dst + q * L::QP, src + q * 2 * L::HW, 2u * L::HW * 2u, bar);
+  } else {
+    bulk_g2s(dst, src, 8u * L::HW * 2u, bar);
+  }
+}
 template <int W, int MODE>
 __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
   using T = __nv_bfloat16;
@@ -486,7 +517,7 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
   auto issue = [&](int64_t t, int s) {
     if (lane == 0 && t < a.ntasks) {
       mbar_arrive_expect_tx(&bars[s], task_bytes);
-      bulk_g2s(slot(s), in + t * 8 * HW, task_bytes, &bars[s]);
+      stage_pairs<W>(slot(s), in + t * 8 * HW, &bars[s]);
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
@@ -507,8 +538,9 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
   };
   int s = 0;
   uint32_t ph = 0;
+  using L = PairLayout<W>;
   for (int64_t t = gw; t < a.ntasks; t += stride) {
-    const int64_t qa = t * 8 + pl, qb = qa + 4;
+    const int64_t qa = t * 8 + L::plane_a(pl), qb = t * 8 + L::plane_b(pl);
     const int ca = (int)(qa % a.C), cb2 = (int)(qb % a.C);
     float2 w2[9];
 #pragma unroll
@@ -518,8 +550,8 @@ __global__ void __launch_bounds__(256) small_fd_pair_kernel(const SArgs a) {
     }
     mbar_wait(&bars[s], ph);
     {  // every lane runs the loop (shuffles); lanes 28-31 recompute lane 27's columns and store nothing
-      const T* pa = slot(s) + pl * HW;
-      const T* pb = pa + 4 * HW;
+      const T* pa = slot(s) + L::off(L::plane_a(pl));
+      const T* pb = slot(s) + L::off(L::plane_b(pl));
       float2 xw[3][V + 2];
 #pragma unroll
       for (int u = 0; u < V + 2; ++u) xw[0][u] = make_float2(0.f, 0.f);
@@ -586,12 +618,13 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
   griddep_wait();
   const uint32_t task_bytes = 8u * HW * (uint32_t)sizeof(T);
   auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  using L = PairLayout<W>;
   auto issue = [&](int n, int s) {
     if (lane == 0 && n < n1) {
       const int64_t off = ((int64_t)n * a.C + cb) * HW;
       mbar_arrive_expect_tx(&bars[s], 2 * task_bytes);
-      bulk_g2s(slot(s), x + off, task_bytes, &bars[s]);
-      bulk_g2s(slot(s) + 8 * HW, dy + off, task_bytes, &bars[s]);
+      stage_pairs<W>(slot(s), x + off, &bars[s]);
+      stage_pairs<W>(slot(s) + L::REGION, dy + off, &bars[s]);
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
@@ -616,10 +649,10 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
   for (int n = n0 + warp; n < n1; n += nwarps) {
     mbar_wait(&bars[s], ph);
     {  // every lane runs the loop (shuffles); lanes 28-31 duplicate lane 27 and are left out of the sums
-      const T* pa = slot(s) + pl * HW;
-      const T* pb = pa + 4 * HW;
-      const T* da = slot(s) + 8 * HW + pl * HW;
-      const T* db = da + 4 * HW;
+      const T* pa = slot(s) + L::off(L::plane_a(pl));
+      const T* pb = slot(s) + L::off(L::plane_b(pl));
+      const T* da = slot(s) + L::REGION + L::off(L::plane_a(pl));
+      const T* db = slot(s) + L::REGION + L::off(L::plane_b(pl));
       float2 xw[3][V + 2];
 #pragma unroll
       for (int u = 0; u < V + 2; ++u) xw[0][u] = make_float2(0.f, 0.f);
@@ -667,8 +700,8 @@ __global__ void __launch_bounds__(256) small_bf_pair_kernel(const SArgs a) {
   __syncthreads();
   float* part = a.ws_part + (int64_t)sl * a.C * 9;
   for (int e = threadIdx.x; e < 8 * 9; e += blockDim.x) {
-    const int ch = e / 9, k = e - ch * 9;  // channel cb + ch
-    const int p = ch & 3, hi = ch >> 2;
+    const int ch = e / 9, k = e - ch * 9;  // channel cb + ch = plane_a(p) (hi 0) or plane_b(p) (hi 1)
+    const int p = L::ADJ ? ch >> 1 : ch & 3, hi = L::ADJ ? ch & 1 : ch >> 2;
     float tot = 0.f;
     for (int wv = 0; wv < nwarps; ++wv) {
       float v = red[(wv * 32 + p * 7) * 18 + hi * 9 + k];
@@ -1115,6 +1148,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   p->ns = stages > 0 ? stages : ns_env;
   const bool bf = pass >= 2;  // bwd_filter or the fused backward
   p->slot_bytes = (uint32_t)(task_bytes + (bf ? dy_bytes : 0));
+  if (pair && g.W == 14) p->slot_bytes = (uint32_t)((bf ? 2 : 1) * PairLayout<14>::REGION * eb);  // padded pairs
   p->S = S;
   p->pair = pair;
   p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
