@@ -313,33 +313,35 @@ class Workload:
             self.fused.append((fused_mode == "all" or (fused_mode == "small" and L.h <= 14)) and L.n > 0 and
                               ops.dwconv_plan(d, 3)["variant_name"] != "none")
         # measured plan selection (tune.py): every candidate launch shape of each pass timed on this
-        # layer's tensors, the fastest kept (before any graph capture)
+        # layer's tensors, the fastest kept as an immutable plan handle (dwconv_plan_create) that every
+        # launch below goes through -- no process-wide plan state is installed or read
         self.tuned = {}
-        if tune:
-            from paper_1803_09926_b200 import tune as tn
-            saved = None
-            if plans_file and os.path.exists(plans_file):
-                with open(plans_file) as f:
-                    saved = json.load(f)
-            for li, L in enumerate(self.layers):
-                if L.n == 0:
-                    continue
-                if saved is not None:  # re-install a saved selection (no timing: e.g. under ncu)
-                    self.tuned[L.name] = saved[L.name]
-                    tn.apply_selection(self.descs[li], self.tuned[L.name])
-                else:
-                    s0 = self.sets[0][li]
-                    self.tuned[L.name] = tn.tune_layer(self.descs[li], s0["x"], s0["dy"], self.w[li],
-                                                       passes=("fwd", "bwd") if self.fused[li] else
-                                                       ("fwd", "bwd_data", "bwd_filter"))
-            torch.cuda.synchronize()
-            if plans_file and saved is None and rank == 0:
-                with open(plans_file, "w") as f:
-                    json.dump(self.tuned, f)
-        wsb = [ops.dwconv_bwd_filter_workspace_bytes(d) for d in self.descs]
-        self.ws = torch.zeros(max([16] + wsb), dtype=torch.uint8, device=dev)
-        self.wsf = torch.zeros(max([16] + [ops.dwconv_bwd_workspace_bytes(d) for d, f in zip(self.descs, self.fused)
-                                           if f]), dtype=torch.uint8, device=dev)
+        self.plans = []
+        from paper_1803_09926_b200 import tune as tn
+        saved = None
+        if tune and plans_file and os.path.exists(plans_file):
+            with open(plans_file) as f:
+                saved = json.load(f)
+        for li, L in enumerate(self.layers):
+            passes = ("fwd", "bwd") if self.fused[li] else ("fwd", "bwd_data", "bwd_filter")
+            if tune and L.n > 0 and saved is not None:  # a saved selection (no timing: e.g. under ncu)
+                self.tuned[L.name] = saved[L.name]
+                self.plans.append(tn.plans_from_selection(self.descs[li], saved[L.name]))
+            elif tune and L.n > 0:
+                s0 = self.sets[0][li]
+                res = tn.tune_layer(self.descs[li], s0["x"], s0["dy"], self.w[li], passes=passes)
+                self.plans.append({k: v["plan"] for k, v in res.items()})
+                self.tuned[L.name] = tn.selection_json(res)
+            else:
+                self.plans.append({k: ops.Plan(self.descs[li], tn.PASSES[k], -1) for k in passes})
+        torch.cuda.synchronize()
+        if tune and plans_file and saved is None and rank == 0:
+            with open(plans_file, "w") as f:
+                json.dump(self.tuned, f)
+        self.ws = torch.zeros(max([16] + [pl["bwd_filter"].workspace_bytes for pl in self.plans if "bwd_filter" in pl]),
+                              dtype=torch.uint8, device=dev)
+        self.wsf = torch.zeros(max([16] + [pl["bwd"].workspace_bytes for pl in self.plans if "bwd" in pl]),
+                               dtype=torch.uint8, device=dev)
         self.footprint = sum(t.numel() * t.element_size() for s in self.sets for b in s for t in b.values())
         self.side = torch.cuda.Stream(device=dev)
         self.stream = torch.cuda.Stream(device=dev)
@@ -358,17 +360,17 @@ class Workload:
                     self.graphs.append(g)
                 torch.cuda.synchronize()
 
-    # -- launches (each one call of the C ABI through the binding)
+    # -- launches (each one call of the C ABI through the binding, on the layer's plan handle)
     def launch(self, pas, li, b):
-        ops, d = self.ops, self.descs[li]
+        pl = self.plans[li][pas]
         if pas == "fwd":
-            ops.dwconv_fwd(d, b["x"], self.w[li], b["y"])
+            pl.fwd(b["x"], self.w[li], b["y"])
         elif pas == "bwd_data":
-            ops.dwconv_bwd_data(d, b["dy"], self.w[li], b["dx"])
+            pl.bwd_data(b["dy"], self.w[li], b["dx"])
         elif pas == "bwd_filter":
-            ops.dwconv_bwd_filter(d, b["x"], b["dy"], self.bucket.views[li], self.ws)
+            pl.bwd_filter(b["x"], b["dy"], self.bucket.views[li], self.ws)
         else:
-            ops.dwconv_bwd(d, b["x"], b["dy"], self.w[li], b["dx"], self.bucket.views[li], self.wsf)
+            pl.bwd(b["x"], b["dy"], self.w[li], b["dx"], self.bucket.views[li], self.wsf)
 
     def kernel_list(self):
         ks = [("fwd", li) for li in range(len(self.layers))]
@@ -482,7 +484,7 @@ class Workload:
     def plans_note(self):
         if not self.tuned:
             return "planner defaults"
-        ch = sum(1 for t in self.tuned.values() for v in t.values() if v["index"] != 0)
+        ch = sum(1 for t in self.tuned.values() for v in t.values() if v["index"] > 0)
         return (f"measured selection (tune.py, before the timed region): {ch} of "
                 f"{sum(len(t) for t in self.tuned.values())} tuned passes changed")
 

@@ -195,11 +195,42 @@ DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* inf
  *   dwconv_plan_select: index into the same list; -1 restores the planner's pick.
  *     Returns DWCONV_ERR_BAD_DESCRIPTOR if the list was not queried first or the
  *     index is out of range.  Both are host-only calls (no launches) and
- *     thread-safe; neither may be called during stream capture of the same pass. */
+ *     thread-safe; neither may be called during stream capture of the same pass.
+ *     dwconv_plan_select changes process-wide behaviour for every later call with
+ *     that descriptor; callers that must not see (or make) such changes use the
+ *     immutable plan handles below (what tune.py and bench.py do). */
 #define DWCONV_MAX_CANDIDATES 32
 DWCONV_API int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, dwconv_plan_info* infos,
                                       int* count);
 DWCONV_API int dwconv_plan_select(const dwconv_desc* d, int pass, int index);
+
+/* Immutable launch plans (stateless alternative to dwconv_plan_select).
+ *   dwconv_plan_create: resolve (d, pass) once on the host, for the CURRENT device:
+ *     candidate = -1 -> the planner's own pick (ignoring any dwconv_plan_select
+ *     selection), k >= 0 -> entry k of dwconv_plan_candidates(d, pass) (the list
+ *     is computed if it was not queried yet; out of range -> BAD_DESCRIPTOR).
+ *     *plan receives a heap object the caller owns (dwconv_plan_destroy frees it).
+ *   dwconv_*_plan: the pass of the plan on caller-owned device buffers, same
+ *     argument meaning, layout, workspace contract, asynchrony and error codes as
+ *     the descriptor calls; the pass must match (else BAD_DESCRIPTOR) and the
+ *     current device must be the plan's (else UNSUPPORTED).  A plan is read-only
+ *     after creation: any number of threads may use one plan concurrently, and
+ *     nothing another call does (dwconv_plan_select included) changes what a plan
+ *     launches -- the calls are stateless and capture-safe.
+ *   dwconv_plan_workspace_bytes: the workspace the plan's bwd_filter / bwd needs.
+ *   dwconv_plan_describe: the plan's launch shape (dwconv_plan_info). */
+typedef struct dwconv_plan_s* dwconv_plan_t;
+DWCONV_API int dwconv_plan_create(const dwconv_desc* d, int pass, int candidate, dwconv_plan_t* plan);
+DWCONV_API void dwconv_plan_destroy(dwconv_plan_t plan);
+DWCONV_API int dwconv_plan_describe(dwconv_plan_t plan, dwconv_plan_info* info);
+DWCONV_API size_t dwconv_plan_workspace_bytes(dwconv_plan_t plan);
+DWCONV_API int dwconv_fwd_plan(dwconv_plan_t plan, const void* x, const void* w, void* y, dwconv_stream stream);
+DWCONV_API int dwconv_bwd_data_plan(dwconv_plan_t plan, const void* dy, const void* w, void* dx,
+                                    dwconv_stream stream);
+DWCONV_API int dwconv_bwd_filter_plan(dwconv_plan_t plan, const void* x, const void* dy, float* dw, void* workspace,
+                                      size_t workspace_bytes, dwconv_stream stream);
+DWCONV_API int dwconv_bwd_plan(dwconv_plan_t plan, const void* x, const void* dy, const void* w, void* dx, float* dw,
+                               void* workspace, size_t workspace_bytes, dwconv_stream stream);
 
 /* Force a kernel family for testing: 0 = automatic (default), 1 = generic only. */
 DWCONV_API int dwconv_set_variant_override(int variant);

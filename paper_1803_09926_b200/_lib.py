@@ -19,7 +19,9 @@ FUNCTIONS = ("dwconv_abi_version", "dwconv_status_string", "dwconv_output_shape"
              "dwconv_bwd_data", "dwconv_bwd_filter_workspace_bytes", "dwconv_bwd_filter",
              "dwconv_bwd_workspace_bytes", "dwconv_bwd",
              "dwconv_workspace_init", "dwconv_plan", "dwconv_plan_candidates", "dwconv_plan_select",
-             "dwconv_set_variant_override")
+             "dwconv_set_variant_override", "dwconv_plan_create", "dwconv_plan_destroy", "dwconv_plan_describe",
+             "dwconv_plan_workspace_bytes", "dwconv_fwd_plan", "dwconv_bwd_data_plan", "dwconv_bwd_filter_plan",
+             "dwconv_bwd_plan")
 MAX_CANDIDATES = 32
 
 
@@ -75,6 +77,19 @@ def load() -> ctypes.CDLL:
     lib.dwconv_plan_candidates.argtypes = [dp, i32, i32, ctypes.POINTER(PlanInfo), ctypes.POINTER(i32)]
     lib.dwconv_plan_select.argtypes = [dp, i32, i32]
     lib.dwconv_set_variant_override.argtypes = [i32]
+    lib.dwconv_plan_create.argtypes = [dp, i32, i32, ctypes.POINTER(vp)]
+    lib.dwconv_plan_destroy.argtypes = [vp]
+    lib.dwconv_plan_destroy.restype = None
+    lib.dwconv_plan_describe.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+    lib.dwconv_plan_workspace_bytes.argtypes = [vp]
+    lib.dwconv_plan_workspace_bytes.restype = sz
+    lib.dwconv_fwd_plan.argtypes = [vp, vp, vp, vp, vp]
+    lib.dwconv_bwd_data_plan.argtypes = [vp, vp, vp, vp, vp]
+    lib.dwconv_bwd_filter_plan.argtypes = [vp, vp, vp, vp, vp, sz, vp]
+    lib.dwconv_bwd_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    for f in ("dwconv_plan_create", "dwconv_plan_describe", "dwconv_fwd_plan", "dwconv_bwd_data_plan",
+              "dwconv_bwd_filter_plan", "dwconv_bwd_plan"):
+        getattr(lib, f).restype = i32
     for f in ("dwconv_output_shape", "dwconv_fwd", "dwconv_bwd_data", "dwconv_bwd_filter", "dwconv_bwd",
               "dwconv_workspace_init", "dwconv_plan", "dwconv_plan_candidates", "dwconv_plan_select",
               "dwconv_set_variant_override"):

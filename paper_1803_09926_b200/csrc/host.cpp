@@ -7,6 +7,7 @@
 #include <climits>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -232,20 +233,25 @@ int dwconv_set_variant_override(int v) {
   return DWCONV_OK;
 }
 
-int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwconv_stream stream) {
-  Geom g;
-  int s = validate(d, &g);
-  if (s != DWCONV_OK) return s;
+}  // extern "C"
+
+namespace {
+
+// ---- dispatch from a resolved (geometry, plan): shared by the descriptor calls
+// (plan chosen per call: the planner's pick or a dwconv_plan_select selection)
+// and the immutable plan handles (dwconv_plan_create).
+int ptr_check_fd(const Geom& g, int pass, const void* in, const void* w, const void* out) {
   const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
-  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) ||
-      (s = check_ptr(y, g.N * g.C * g.m * g.Ho * g.Wo, eb)))
+  const int64_t nx = g.N * g.C * g.H * g.W, ny = g.N * g.C * g.m * g.Ho * g.Wo;
+  int s;
+  if ((s = check_ptr(in, pass == DWCONV_PASS_FWD ? nx : ny, eb)) || (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) ||
+      (s = check_ptr(out, pass == DWCONV_PASS_FWD ? ny : nx, eb)))
     return s;
+  return DWCONV_OK;
+}
+
+int run_fwd(const Geom& g, const Plan& p, const void* x, const void* w, void* y, cudaStream_t st) {
   if (g.N == 0) return DWCONV_OK;
-  DevInfo di;
-  if ((s = check_device(&di))) return s;
-  Plan p;
-  make_plan(g, DWCONV_PASS_FWD, di, &p);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // the NCHW kernels store y with V-wide vector stores straight from registers
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(y) % 16) == 0 &&
       (!p.chunk.small || (reinterpret_cast<uintptr_t>(x) % 16) == 0))
@@ -262,20 +268,8 @@ int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwco
   return cuda_status(dwk::launch_generic_fwd(g, x, w, y, st));
 }
 
-int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* dx, dwconv_stream stream) {
-  Geom g;
-  int s = validate(d, &g);
-  if (s != DWCONV_OK) return s;
-  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
-  if ((s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) || (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) ||
-      (s = check_ptr(dx, g.N * g.C * g.H * g.W, eb)))
-    return s;
+int run_bwd_data(const Geom& g, const Plan& p, const void* dy, const void* w, void* dx, cudaStream_t st) {
   if (g.N == 0) return DWCONV_OK;
-  DevInfo di;
-  if ((s = check_device(&di))) return s;
-  Plan p;
-  make_plan(g, DWCONV_PASS_BWD_DATA, di, &p);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // the NCHW kernels store dx with vector stores straight from registers
   if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0 &&
       (!p.chunk.small || (reinterpret_cast<uintptr_t>(dy) % 16) == 0))
@@ -292,13 +286,7 @@ int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* d
   return cuda_status(dwk::launch_generic_bwd_data(g, dy, w, dx, st));
 }
 
-size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
-  Geom g;
-  if (validate(d, &g) != DWCONV_OK) return 0;
-  DevInfo di;
-  if (check_device(&di) != DWCONV_OK) return 0;
-  Plan p;
-  make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
+size_t bf_workspace_bytes(const Plan& p) {
   if (p.variant == DWCONV_VARIANT_NHWC_TILE) return p.nhwc.ws_bytes;
   if (p.variant == DWCONV_VARIANT_NHWC_GEN) return p.gen.ws_bytes;
   if (p.variant == DWCONV_VARIANT_NHWC_TMA)  // either NHWC kernel may run (pointer alignment)
@@ -306,50 +294,131 @@ size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
   return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? p.chunk.ws_bytes : 0;
 }
 
+int ws_check(const void* ws, size_t have, size_t need) {
+  if (have < need) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
+  if (need == 0) return DWCONV_OK;
+  if (!ws) return DWCONV_ERR_NULL_POINTER;
+  if (reinterpret_cast<uintptr_t>(ws) % 16) return DWCONV_ERR_MISALIGNED;
+  return DWCONV_OK;
+}
+
+int run_bwd_filter(const Geom& g, const Plan& p, const void* x, const void* dy, float* dw, void* workspace,
+                   size_t workspace_bytes, cudaStream_t st) {
+  if (g.N == 0) return cuda_status(cudaMemsetAsync(dw, 0, (size_t)(g.C * g.m * g.kh * g.kw) * 4, st));
+  int s;
+  // the register-direct variant needs 16-B aligned x and dy (vector loads)
+  const bool direct_ok = !(p.chunk.direct || p.chunk.small) ||
+                         ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0;
+  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && direct_ok) {
+    if ((s = ws_check(workspace, workspace_bytes, p.chunk.ws_bytes))) return s;
+    return cuda_status(dwk::launch_nchw_bwd_filter(g, p.chunk, x, dy, dw, workspace, st));
+  }
+  if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(x, dy)) {
+    if ((s = ws_check(workspace, workspace_bytes, p.tma.ws_bytes))) return s;
+    return cuda_status(dwk::launch_nhwc_tma_bf(g, p.tma, x, dy, dw, workspace, st));
+  }
+  if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
+      nhwc_aligned(g, x, dy)) {
+    if ((s = ws_check(workspace, workspace_bytes, p.nhwc.ws_bytes))) return s;
+    return cuda_status(dwk::launch_nhwc_bwd_filter(g, p.nhwc, x, dy, dw, workspace, st));
+  }
+  if (p.variant == DWCONV_VARIANT_NHWC_GEN && tma_aligned(x, dy)) {
+    if ((s = ws_check(workspace, workspace_bytes, p.gen.ws_bytes))) return s;
+    return cuda_status(dwk::launch_nhwc_gen_bf(g, p.gen, x, dy, dw, workspace, st));
+  }
+  return cuda_status(dwk::launch_generic_bwd_filter(g, x, dy, dw, st));
+}
+
+// fused backward: pf = the PASS_BWD plan; pd / pb = the two-call fallback plans
+int run_bwd(const Geom& g, const Plan& pf, const Plan& pd, const Plan& pb, const void* x, const void* dy,
+            const void* w, void* dx, float* dw, void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  int s;
+  // the fused kernel stores dx with vector stores straight from registers
+  if (g.N > 0 && pf.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0 &&
+      (!pf.chunk.small || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0)) {
+    if ((s = ws_check(workspace, workspace_bytes, pf.chunk.ws_bytes))) return s;
+    return cuda_status(dwk::launch_nchw_bwd_fused(g, pf.chunk, x, dy, w, dx, dw, workspace, st));
+  }
+  if ((s = run_bwd_data(g, pd, dy, w, dx, st))) return s;
+  return run_bwd_filter(g, pb, x, dy, dw, workspace, workspace_bytes, st);
+}
+
+size_t bwd_workspace_bytes(const Plan& pf, const Plan& pb) {
+  const size_t two = bf_workspace_bytes(pb);
+  return pf.variant == DWCONV_VARIANT_NCHW_CHUNK ? std::max(pf.chunk.ws_bytes, two) : two;
+}
+
+}  // namespace
+
+// Immutable launch plan: geometry, pass and the resolved kernel plan(s), fixed at
+// creation; calls through it read nothing that any other call can change.
+struct dwconv_plan_s {
+  Geom g;
+  int pass = 0;
+  int device = 0;
+  int candidate = -1;
+  Plan p;       // the pass's plan (PASS_BWD: the fused plan)
+  Plan pd, pb;  // PASS_BWD: the two-call fallback's bwd_data / bwd_filter plans (planner defaults)
+};
+
+extern "C" {
+
+int dwconv_fwd(const dwconv_desc* d, const void* x, const void* w, void* y, dwconv_stream stream) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if ((s = ptr_check_fd(g, DWCONV_PASS_FWD, x, w, y))) return s;
+  if (g.N == 0) return DWCONV_OK;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  Plan p;
+  make_plan(g, DWCONV_PASS_FWD, di, &p);
+  return run_fwd(g, p, x, w, y, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dwconv_bwd_data(const dwconv_desc* d, const void* dy, const void* w, void* dx, dwconv_stream stream) {
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if ((s = ptr_check_fd(g, DWCONV_PASS_BWD_DATA, dy, w, dx))) return s;
+  if (g.N == 0) return DWCONV_OK;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  Plan p;
+  make_plan(g, DWCONV_PASS_BWD_DATA, di, &p);
+  return run_bwd_data(g, p, dy, w, dx, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t dwconv_bwd_filter_workspace_bytes(const dwconv_desc* d) {
+  Geom g;
+  if (validate(d, &g) != DWCONV_OK) return 0;
+  DevInfo di;
+  if (check_device(&di) != DWCONV_OK) return 0;
+  Plan p;
+  make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
+  return bf_workspace_bytes(p);
+}
+
+static int ptr_check_bf(const Geom& g, const void* x, const void* dy, const float* dw) {
+  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+  int s;
+  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) ||
+      (s = check_ptr(dw, g.C * g.m * g.kh * g.kw, 4)))
+    return s;
+  return DWCONV_OK;
+}
+
 int dwconv_bwd_filter(const dwconv_desc* d, const void* x, const void* dy, float* dw, void* workspace,
                       size_t workspace_bytes, dwconv_stream stream) {
   Geom g;
   int s = validate(d, &g);
   if (s != DWCONV_OK) return s;
-  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
-  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) ||
-      (s = check_ptr(dw, g.C * g.m * g.kh * g.kw, 4)))
-    return s;
+  if ((s = ptr_check_bf(g, x, dy, dw))) return s;
   DevInfo di;
   if ((s = check_device(&di))) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (g.N == 0) return cuda_status(cudaMemsetAsync(dw, 0, (size_t)(g.C * g.m * g.kh * g.kw) * 4, st));
   Plan p;
-  make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
-  // the register-direct variant needs 16-B aligned x and dy (vector loads)
-  const bool direct_ok = !(p.chunk.direct || p.chunk.small) ||
-                         ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0;
-  if (p.variant == DWCONV_VARIANT_NCHW_CHUNK && direct_ok) {
-    if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
-    if (!workspace) return DWCONV_ERR_NULL_POINTER;
-    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
-    return cuda_status(dwk::launch_nchw_bwd_filter(g, p.chunk, x, dy, dw, workspace, st));
-  }
-  if (p.variant == DWCONV_VARIANT_NHWC_TMA && tma_aligned(x, dy)) {
-    if (workspace_bytes < p.tma.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
-    if (!workspace) return DWCONV_ERR_NULL_POINTER;
-    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
-    return cuda_status(dwk::launch_nhwc_tma_bf(g, p.tma, x, dy, dw, workspace, st));
-  }
-  if ((p.variant == DWCONV_VARIANT_NHWC_TILE || p.variant == DWCONV_VARIANT_NHWC_TMA) && p.nhwc.grid > 0 &&
-      nhwc_aligned(g, x, dy)) {
-    if (workspace_bytes < p.nhwc.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
-    if (!workspace) return DWCONV_ERR_NULL_POINTER;
-    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
-    return cuda_status(dwk::launch_nhwc_bwd_filter(g, p.nhwc, x, dy, dw, workspace, st));
-  }
-  if (p.variant == DWCONV_VARIANT_NHWC_GEN && tma_aligned(x, dy)) {
-    if (workspace_bytes < p.gen.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
-    if (!workspace) return DWCONV_ERR_NULL_POINTER;
-    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
-    return cuda_status(dwk::launch_nhwc_gen_bf(g, p.gen, x, dy, dw, workspace, st));
-  }
-  return cuda_status(dwk::launch_generic_bwd_filter(g, x, dy, dw, st));
+  if (g.N > 0) make_plan(g, DWCONV_PASS_BWD_FILTER, di, &p);
+  return run_bwd_filter(g, p, x, dy, dw, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t dwconv_bwd_workspace_bytes(const dwconv_desc* d) {
@@ -357,10 +426,10 @@ size_t dwconv_bwd_workspace_bytes(const dwconv_desc* d) {
   if (validate(d, &g) != DWCONV_OK) return 0;
   DevInfo di;
   if (check_device(&di) != DWCONV_OK) return 0;
-  Plan p;
-  make_plan(g, DWCONV_PASS_BWD, di, &p);
-  const size_t two = dwconv_bwd_filter_workspace_bytes(d);
-  return p.variant == DWCONV_VARIANT_NCHW_CHUNK ? std::max(p.chunk.ws_bytes, two) : two;
+  Plan pf, pb;
+  make_plan(g, DWCONV_PASS_BWD, di, &pf);
+  make_plan(g, DWCONV_PASS_BWD_FILTER, di, &pb);
+  return bwd_workspace_bytes(pf, pb);
 }
 
 int dwconv_bwd(const dwconv_desc* d, const void* x, const void* dy, const void* w, void* dx, float* dw,
@@ -368,26 +437,17 @@ int dwconv_bwd(const dwconv_desc* d, const void* x, const void* dy, const void* 
   Geom g;
   int s = validate(d, &g);
   if (s != DWCONV_OK) return s;
-  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
-  if ((s = check_ptr(x, g.N * g.C * g.H * g.W, eb)) || (s = check_ptr(dy, g.N * g.C * g.m * g.Ho * g.Wo, eb)) ||
-      (s = check_ptr(w, g.C * g.m * g.kh * g.kw, eb)) || (s = check_ptr(dx, g.N * g.C * g.H * g.W, eb)) ||
-      (s = check_ptr(dw, g.C * g.m * g.kh * g.kw, 4)))
-    return s;
+  if ((s = ptr_check_bf(g, x, dy, dw)) || (s = ptr_check_fd(g, DWCONV_PASS_BWD_DATA, dy, w, dx))) return s;
   DevInfo di;
   if ((s = check_device(&di))) return s;
-  Plan p;
-  if (g.N > 0) make_plan(g, DWCONV_PASS_BWD, di, &p);
-  // the fused kernel stores dx with vector stores straight from registers
-  if (g.N > 0 && p.variant == DWCONV_VARIANT_NCHW_CHUNK && (reinterpret_cast<uintptr_t>(dx) % 16) == 0 &&
-      (!p.chunk.small || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) % 16) == 0)) {
-    if (workspace_bytes < p.chunk.ws_bytes) return DWCONV_ERR_WORKSPACE_TOO_SMALL;
-    if (!workspace) return DWCONV_ERR_NULL_POINTER;
-    if (reinterpret_cast<uintptr_t>(workspace) % 16) return DWCONV_ERR_MISALIGNED;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    return cuda_status(dwk::launch_nchw_bwd_fused(g, p.chunk, x, dy, w, dx, dw, workspace, st));
+  Plan pf, pd, pb;
+  if (g.N > 0) {
+    make_plan(g, DWCONV_PASS_BWD, di, &pf);
+    make_plan(g, DWCONV_PASS_BWD_DATA, di, &pd);
+    make_plan(g, DWCONV_PASS_BWD_FILTER, di, &pb);
   }
-  if ((s = dwconv_bwd_data(d, dy, w, dx, stream))) return s;
-  return dwconv_bwd_filter(d, x, dy, dw, workspace, workspace_bytes, stream);
+  return run_bwd(g, pf, pd, pb, x, dy, w, dx, dw, workspace, workspace_bytes,
+                 reinterpret_cast<cudaStream_t>(stream));
 }
 
 int dwconv_workspace_init(void* workspace, size_t workspace_bytes, dwconv_stream stream) {
@@ -652,6 +712,101 @@ int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info) {
   make_plan(g, pass, di, &p);
   fill_info(g, p, pass, info);
   return DWCONV_OK;
+}
+
+// ---- immutable plan handles
+int dwconv_plan_create(const dwconv_desc* d, int pass, int candidate, dwconv_plan_t* out) {
+  if (!out) return DWCONV_ERR_NULL_POINTER;
+  *out = nullptr;
+  Geom g;
+  int s = validate(d, &g);
+  if (s != DWCONV_OK) return s;
+  if (pass < DWCONV_PASS_FWD || pass > DWCONV_PASS_BWD || candidate < -1) return DWCONV_ERR_BAD_DESCRIPTOR;
+  DevInfo di;
+  if ((s = check_device(&di))) return s;
+  auto* h = new (std::nothrow) dwconv_plan_s;
+  if (!h) return DWCONV_ERR_CUDA;
+  h->g = g;
+  h->pass = pass;
+  h->candidate = candidate;
+  cudaGetDevice(&h->device);
+  if (g.N > 0) {
+    if (candidate < 0) {
+      make_plan_uncached(g, pass, di, &h->p);  // the planner's own pick, whatever dwconv_plan_select installed
+    } else {
+      int count = 0;
+      if ((s = dwconv_plan_candidates(d, pass, 0, nullptr, &count))) { delete h; return s; }
+      const PlanKey key = plan_key(g, pass, di);
+      std::lock_guard<std::mutex> lk(g_sel_mu);
+      auto it = g_candidates.find(key);
+      if (it == g_candidates.end() || candidate >= (int)it->second.size()) {
+        delete h;
+        return DWCONV_ERR_BAD_DESCRIPTOR;
+      }
+      h->p = it->second[(size_t)candidate];
+    }
+    if (pass == DWCONV_PASS_BWD) {
+      make_plan_uncached(g, DWCONV_PASS_BWD_DATA, di, &h->pd);
+      make_plan_uncached(g, DWCONV_PASS_BWD_FILTER, di, &h->pb);
+    }
+  }
+  *out = h;
+  return DWCONV_OK;
+}
+
+void dwconv_plan_destroy(dwconv_plan_t plan) { delete plan; }
+
+static int plan_ready(dwconv_plan_t h, int pass) {
+  if (!h) return DWCONV_ERR_NULL_POINTER;
+  if (h->pass != pass) return DWCONV_ERR_BAD_DESCRIPTOR;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DWCONV_ERR_CUDA;
+  return dev == h->device ? DWCONV_OK : DWCONV_ERR_UNSUPPORTED;
+}
+
+int dwconv_plan_describe(dwconv_plan_t h, dwconv_plan_info* info) {
+  if (!h || !info) return DWCONV_ERR_NULL_POINTER;
+  fill_info(h->g, h->p, h->pass, info);
+  if (h->pass == DWCONV_PASS_BWD) info->workspace_bytes = (int64_t)bwd_workspace_bytes(h->p, h->pb);
+  if (h->pass == DWCONV_PASS_BWD_FILTER) info->workspace_bytes = (int64_t)bf_workspace_bytes(h->p);
+  return DWCONV_OK;
+}
+
+size_t dwconv_plan_workspace_bytes(dwconv_plan_t h) {
+  if (!h) return 0;
+  if (h->pass == DWCONV_PASS_BWD_FILTER) return bf_workspace_bytes(h->p);
+  if (h->pass == DWCONV_PASS_BWD) return bwd_workspace_bytes(h->p, h->pb);
+  return 0;
+}
+
+int dwconv_fwd_plan(dwconv_plan_t h, const void* x, const void* w, void* y, dwconv_stream stream) {
+  int s;
+  if ((s = plan_ready(h, DWCONV_PASS_FWD)) || (s = ptr_check_fd(h->g, DWCONV_PASS_FWD, x, w, y))) return s;
+  return run_fwd(h->g, h->p, x, w, y, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dwconv_bwd_data_plan(dwconv_plan_t h, const void* dy, const void* w, void* dx, dwconv_stream stream) {
+  int s;
+  if ((s = plan_ready(h, DWCONV_PASS_BWD_DATA)) || (s = ptr_check_fd(h->g, DWCONV_PASS_BWD_DATA, dy, w, dx)))
+    return s;
+  return run_bwd_data(h->g, h->p, dy, w, dx, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dwconv_bwd_filter_plan(dwconv_plan_t h, const void* x, const void* dy, float* dw, void* workspace,
+                           size_t workspace_bytes, dwconv_stream stream) {
+  int s;
+  if ((s = plan_ready(h, DWCONV_PASS_BWD_FILTER)) || (s = ptr_check_bf(h->g, x, dy, dw))) return s;
+  return run_bwd_filter(h->g, h->p, x, dy, dw, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dwconv_bwd_plan(dwconv_plan_t h, const void* x, const void* dy, const void* w, void* dx, float* dw,
+                    void* workspace, size_t workspace_bytes, dwconv_stream stream) {
+  int s;
+  if ((s = plan_ready(h, DWCONV_PASS_BWD)) || (s = ptr_check_bf(h->g, x, dy, dw)) ||
+      (s = ptr_check_fd(h->g, DWCONV_PASS_BWD_DATA, dy, w, dx)))
+    return s;
+  return run_bwd(h->g, h->p, h->pd, h->pb, x, dy, w, dx, dw, workspace, workspace_bytes,
+                 reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

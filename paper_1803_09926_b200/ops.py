@@ -196,6 +196,68 @@ def dwconv_plan_select(d: Desc, pass_: int, index: int) -> None:
     _lib.check(_lib.load().dwconv_plan_select(ctypes.byref(d), pass_, index), "dwconv_plan_select")
 
 
+class Plan:
+    """An immutable launch plan (``dwconv_plan_create``): descriptor + pass + candidate resolved once.
+
+    ``candidate=-1`` is the planner's own pick; ``k >= 0`` is entry k of ``dwconv_plan_candidates``.  Calls
+    through a plan never read process-wide state (``dwconv_plan_select`` does not affect them), so plans
+    are safe to share between threads and to capture in CUDA graphs.
+    """
+
+    def __init__(self, d: Desc, pass_: int, candidate: int = -1):
+        self.desc, self.pass_, self.candidate = d, pass_, candidate
+        h = ctypes.c_void_p()
+        self._lib = _lib.load()
+        _lib.check(self._lib.dwconv_plan_create(ctypes.byref(d), pass_, candidate, ctypes.byref(h)),
+                   "dwconv_plan_create")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.dwconv_plan_destroy(h)
+            self._h = None
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self._lib.dwconv_plan_workspace_bytes(self._h))
+
+    def describe(self) -> Dict[str, int]:
+        info = PlanInfo()
+        _lib.check(self._lib.dwconv_plan_describe(self._h, ctypes.byref(info)), "dwconv_plan_describe")
+        out = {f: getattr(info, f) for f, _ in PlanInfo._fields_}
+        out["variant_name"] = _lib.VARIANTS.get(info.variant, "?")
+        return out
+
+    def fwd(self, x: torch.Tensor, w: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+        _check_tensors(self.desc, x=x, w=w, y=y)
+        with torch.cuda.device(x.device):
+            _lib.check(self._lib.dwconv_fwd_plan(self._h, _ptr(x), _ptr(w), _ptr(y), _stream(stream)),
+                       "dwconv_fwd_plan")
+
+    def bwd_data(self, dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, stream=None) -> None:
+        _check_tensors(self.desc, dy=dy, w=w, dx=dx)
+        with torch.cuda.device(dy.device):
+            _lib.check(self._lib.dwconv_bwd_data_plan(self._h, _ptr(dy), _ptr(w), _ptr(dx), _stream(stream)),
+                       "dwconv_bwd_data_plan")
+
+    def bwd_filter(self, x: torch.Tensor, dy: torch.Tensor, dw: torch.Tensor, workspace: Optional[torch.Tensor],
+                   stream=None) -> None:
+        _check_tensors(self.desc, x=x, dy=dy, dw=dw)
+        nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        with torch.cuda.device(x.device):
+            _lib.check(self._lib.dwconv_bwd_filter_plan(self._h, _ptr(x), _ptr(dy), _ptr(dw), _ptr(workspace),
+                                                        nbytes, _stream(stream)), "dwconv_bwd_filter_plan")
+
+    def bwd(self, x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, dw: torch.Tensor,
+            workspace: Optional[torch.Tensor], stream=None) -> None:
+        _check_tensors(self.desc, x=x, dy=dy, w=w, dx=dx, dw=dw)
+        nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        with torch.cuda.device(x.device):
+            _lib.check(self._lib.dwconv_bwd_plan(self._h, _ptr(x), _ptr(dy), _ptr(w), _ptr(dx), _ptr(dw),
+                                                 _ptr(workspace), nbytes, _stream(stream)), "dwconv_bwd_plan")
+
+
 def dwconv_set_variant_override(v: int) -> None:
     _lib.check(_lib.load().dwconv_set_variant_override(v), "dwconv_set_variant_override")
 

@@ -205,16 +205,60 @@ def test_tune_layer_selects_a_candidate():
     x = torch.randn(L.n, L.c, L.h, L.w, device="cuda")
     dy = torch.randn(L.n, L.c, L.ho, L.wo, device="cuda")
     w = torch.randn(L.c, L.k, L.k, device="cuda")
+    before = {p: ops.dwconv_plan(d, p) for p in range(3)}
     res = tune.tune_layer(d, x, dy, w)
-    try:
-        assert set(res) == {"fwd", "bwd_data", "bwd_filter"}
-        for name, r in res.items():
-            assert 0 <= r["index"] < r["candidates"] and r["us"] <= r["default_us"]
-            info = ops.dwconv_plan(d, tune.PASSES[name])
-            assert info["grid"] == r["grid"] and info["block"] == r["block"]
-    finally:
-        for p in range(3):
-            ops.dwconv_plan_select(d, p, -1)
+    assert set(res) == {"fwd", "bwd_data", "bwd_filter"}
+    for name, r in res.items():
+        assert 0 <= r["index"] < r["candidates"] and r["us"] <= r["default_us"]
+        info = r["plan"].describe()
+        assert info["grid"] == r["grid"] and info["block"] == r["block"]
+        # tuning installs nothing process-wide: the descriptor API still runs the planner's pick
+        assert ops.dwconv_plan(d, tune.PASSES[name]) == before[tune.PASSES[name]]
+
+
+def test_plan_handles_match_selected_descriptor_calls_and_ignore_selection():
+    """dwconv_plan_create(d, pass, k) launches exactly what dwconv_plan_select(d, pass, k) + the descriptor call
+    launches (bitwise equal outputs), and a later dwconv_plan_select does not change what a handle runs."""
+    L = [l for l in synth.mobilenet_v1_dw(8) if l.name == "dw6"][0]
+    d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, NCHW, F32)
+    x = torch.randn(L.n, L.c, L.h, L.w, device="cuda")
+    dy = torch.randn(L.n, L.c, L.ho, L.wo, device="cuda")
+    w = torch.randn(L.c, L.k, L.k, device="cuda")
+    for pas in (0, 1, 2):
+        cands = ops.dwconv_plan_candidates(d, pas)
+        assert len(cands) >= 2
+        for k in (0, len(cands) // 2, len(cands) - 1):
+            pl = ops.Plan(d, pas, k)
+            assert pl.describe()["grid"] == cands[k]["grid"]
+            other = (k + 1) % len(cands)
+            ws = torch.zeros(max(16, pl.workspace_bytes, cands[other]["workspace_bytes"]), dtype=torch.uint8,
+                             device="cuda")
+            try:
+                ops.dwconv_plan_select(d, pas, k)
+                if pas == 0:
+                    a, b = torch.empty_like(dy), torch.empty_like(dy)
+                    ops.dwconv_fwd(d, x, w, a)
+                    ops.dwconv_plan_select(d, pas, other)
+                    pl.fwd(x, w, b)
+                elif pas == 1:
+                    a, b = torch.empty_like(x), torch.empty_like(x)
+                    ops.dwconv_bwd_data(d, dy, w, a)
+                    ops.dwconv_plan_select(d, pas, other)
+                    pl.bwd_data(dy, w, b)
+                else:
+                    a, b = torch.empty(w.shape, device="cuda"), torch.empty(w.shape, device="cuda")
+                    ops.dwconv_bwd_filter(d, x, dy, a, ws)
+                    ops.dwconv_plan_select(d, pas, other)
+                    pl.bwd_filter(x, dy, b, ws)
+                torch.cuda.synchronize()
+                assert torch.equal(a, b), (pas, k)
+            finally:
+                ops.dwconv_plan_select(d, pas, -1)
+    # a pass mismatch is an error, not a silent launch
+    pl = ops.Plan(d, 0, -1)
+    with pytest.raises(RuntimeError):
+        ops._lib.check(ops._lib.load().dwconv_bwd_data_plan(pl._h, dy.data_ptr(), w.data_ptr(), x.data_ptr(),
+                                                            None), "mismatch")
 
 
 # Edge shapes for the small-plane / band / TMA candidates at small batch: one

@@ -27,6 +27,9 @@ SETS = {
     "cfg4": [(64, 128, 56, 56, 2, 3, 1, 1), (64, 128, 56, 56, 4, 3, 1, 1), (64, 128, 56, 56, 1, 5, 1, 2),
              (64, 128, 56, 56, 1, 7, 1, 3), (64, 512, 56, 56, 1, 3, 2, 1), (64, 512, 56, 56, 1, 5, 2, 2),
              (64, 512, 56, 56, 1, 7, 2, 3)],
+    # MobileNet-v1 layers at batch 128 (the >= 70 % target set): large planes and the 14x14 / 7x7 layers
+    "mb128": [(128, 32, 112, 112, 1, 3, 1, 1), (128, 64, 112, 112, 1, 3, 2, 1), (128, 128, 56, 56, 1, 3, 1, 1),
+              (128, 512, 14, 14, 1, 3, 1, 1), (128, 512, 14, 14, 1, 3, 2, 1), (128, 1024, 7, 7, 1, 3, 1, 1)],
     # the group-size sweep: stride-1 K = 3 / 5 / 7 on 56x56x128 (b64) and a MobileNet 3x3 layer (dw6, b128)
     "sweep": [(64, 128, 56, 56, 1, 3, 1, 1), (64, 128, 56, 56, 1, 5, 1, 2), (64, 128, 56, 56, 1, 7, 1, 3),
               (128, 128, 56, 56, 1, 3, 1, 1), (128, 512, 14, 14, 1, 3, 1, 1)],
