@@ -67,6 +67,9 @@ def parse(argv=None):
     ap.add_argument("--no-b128", action="store_true", help="skip the batch-128 target-set workloads (N=1 only)")
     ap.add_argument("--b128-steps", type=int, default=50)
     ap.add_argument("--extra", action="store_true", help="add per-layer kernel table to the JSON line")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend at N > 1 (gloo + --one-device: exercise the N > 1 path on one GPU)")
+    ap.add_argument("--one-device", action="store_true", help="put every rank on cuda:0 (test mode)")
     return ap.parse_args(argv)
 
 
@@ -520,10 +523,15 @@ def main(argv=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.one_device:  # test mode: every rank on cuda:0 (NCCL refuses that; use --dist-backend gloo)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     strong = args.global_batch > 0
     if strong:
         _, batch = dp.shard_batch(args.global_batch, world, rank)
@@ -579,6 +587,7 @@ def main(argv=None):
         busbw = 2.0 * (world - 1) / world * wl.bucket.nbytes / (ar_us * 1e-6) / 1e9
         comm = {"allreduce_us": ar_us, "bytes": wl.bucket.nbytes, "bus_gbs": busbw,
                 "nvlink_frac": busbw / NVLINK_GBS_PER_DIR, "share_of_step": ar_us * 1e-3 / ms,
+                "backend": args.dist_backend + (" (test mode: every rank on cuda:0)" if args.one_device else ""),
                 "nccl_algo": os.environ.get("NCCL_ALGO", "auto"), "nccl_proto": os.environ.get("NCCL_PROTO", "auto"),
                 "note": "latency-bound: 178,560 B per step (SURVEY §8(e))"}
 
@@ -646,7 +655,7 @@ def main(argv=None):
                "path": "python binding -> C ABI eager calls; pinned host->device copies of x, dy, w for all "
                        "13 layers and device->host copy of the dw bucket inside the timed region"}
 
-    gpu_launches = len(wl.kernel_list()) * args.steps
+    gpu_launches = len(wl.kernel_list()) * args.steps * world  # every rank launches the same step
     plans_note = wl.plans_note()
     footprint = wl.footprint
     nfused = sum(wl.fused)
