@@ -794,9 +794,108 @@ __global__ void __launch_bounds__(256) small_fwd2_kernel(const SArgs a) {
   if (!a.early_pdl) griddep_launch_dependents();
 }
 
-template <class T, int W>
+// stride-2 input gradient (polyphase): dx plane W x W from the dy plane Wo = W/2.
+// With pad 1, dx[ih, iw] = sum_{i,j} w[i,j] dy[(ih+1-i)/2, (iw+1-j)/2] over exact
+// divisions (reading R9), so per dy position (a, b):
+//   dx[2a,   2b  ] = w11 dy[a,b]
+//   dx[2a,   2b+1] = w10 dy[a,b+1] + w12 dy[a,b]
+//   dx[2a+1, 2b  ] = w01 dy[a+1,b] + w21 dy[a,b]
+//   dx[2a+1, 2b+1] = w00 dy[a+1,b+1] + w02 dy[a+1,b] + w20 dy[a,b+1] + w22 dy[a,b]
+// (dy = 0 past the plane).  Warp task = TP dy planes (one bulk copy; TP = 8 when 4
+// planes are not a 16-B multiple: bf16 7x7); lane (plane, column group) owns V dy
+// columns and the 2V dx columns they feed, walks the dy rows with a 2-row window
+// (the right halo column from the next lane by shuffle) and stores two dx rows
+// per dy row straight from registers; TP = 8 runs the lanes over two plane quads.
+template <class T, int W, int TP = 4>
+__global__ void __launch_bounds__(256) small_bd2_kernel(const SArgs a) {
+  constexpr int Wo = W / 2, V = Wo / 7, HWo = Wo * Wo, HW = W * W;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const int pl = min(lane / 7, 3), cg = (lane < 28) ? lane - (lane / 7) * 7 : 6;  // lanes 28-31 shadow lane 27
+  const bool live = lane < 28;
+  const int c0 = cg * V;
+  const bool rgt = c0 + V < Wo;
+  const T* __restrict__ in = static_cast<const T*>(a.in);
+  T* __restrict__ out = static_cast<T*>(a.out);
+  const T* __restrict__ wt = static_cast<const T*>(a.w);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * nwarps;
+  const uint32_t task_bytes = (uint32_t)TP * HWo * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int64_t t, int s) {
+    if (lane == 0 && t < a.ntasks) {
+      mbar_arrive_expect_tx(&bars[s], task_bytes);
+      bulk_g2s(slot(s), in + t * TP * HWo, task_bytes, &bars[s]);
+    }
+  };
+  for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
+  // one dy row: the lane's V columns and the next lane's first column (all lanes call this)
+  auto ldrow = [&](const T* row, float* d) {
+    float v[V];
+    VecIO<T, V>::load(row + c0, v);
+#pragma unroll
+    for (int u = 0; u < V; ++u) d[u] = v[u];
+    const float r = __shfl_down_sync(0xffffffffu, v[0], 1);
+    d[V] = rgt ? r : 0.f;
+  };
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = gw; t < a.ntasks; t += stride) {
+    mbar_wait(&bars[s], ph);
+#pragma unroll 1
+    for (int quad = 0; quad < TP / 4; ++quad) {  // every lane runs the loop (shuffles); only live lanes store
+      const int64_t q = t * TP + quad * 4 + pl;
+      const int c = (int)(q % a.C);
+      float w[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) w[k] = Elem<T>::ldg(wt + (int64_t)c * 9 + k);
+      const T* pln = slot(s) + (quad * 4 + pl) * HWo;
+      T* po = out + q * HW + 2 * c0;
+      float cur[V + 1], nxt[V + 1];
+      ldrow(pln, cur);
+#pragma unroll
+      for (int r = 0; r < Wo; ++r) {
+        if (r + 1 < Wo) ldrow(pln + (r + 1) * Wo, nxt);
+        else
+#pragma unroll
+          for (int u = 0; u <= V; ++u) nxt[u] = 0.f;
+        float e0[2 * V], e1[2 * V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          const float d00 = cur[u], d01 = cur[u + 1], d10 = nxt[u], d11 = nxt[u + 1];
+          e0[2 * u] = w[4] * d00;
+          e0[2 * u + 1] = fmaf(w[5], d00, w[3] * d01);
+          e1[2 * u] = fmaf(w[7], d00, w[1] * d10);
+          e1[2 * u + 1] = fmaf(w[8], d00, fmaf(w[6], d01, fmaf(w[2], d10, w[0] * d11)));
+        }
+        if (live) {
+          VecIO<T, 2 * V>::store(po + (2 * r) * W, e0);
+          VecIO<T, 2 * V>::store(po + (2 * r + 1) * W, e1);
+        }
+#pragma unroll
+        for (int u = 0; u <= V; ++u) cur[u] = nxt[u];
+      }
+    }
+    __syncwarp();
+    issue(t + a.ns * stride, s);
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  if (!a.early_pdl) griddep_launch_dependents();
+}
+
+template <class T, int W, int TP = 4>  // TP channels per group (8: bf16 7x7 dy planes, 4 x 98 B is not a 16-B multiple)
 __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
-  constexpr int Wo = W / 2, V = Wo / 7, HW = W * W, HWo = Wo * Wo, NXW = 2 * V + 1;
+  constexpr int Wo = W / 2, V = Wo / 7, HW = W * W, HWo = Wo * Wo, NXW = 2 * V + 1, NQ = TP / 4;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -807,7 +906,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   const bool live = lane < 28;
   const int c0 = cg * V;
   const int g = blockIdx.x % a.groups, sl = blockIdx.x / a.groups;
-  const int cb = g * 4;
+  const int cb = g * TP;
   const int n0 = sl * a.nps, n1 = min(a.N, n0 + a.nps);
   const T* __restrict__ x = static_cast<const T*>(a.in);
   const T* __restrict__ dy = static_cast<const T*>(a.in2);
@@ -817,27 +916,30 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   }
   __syncwarp();
   griddep_wait();
-  const uint32_t xbytes = 4u * HW * (uint32_t)sizeof(T), dbytes = 4u * HWo * (uint32_t)sizeof(T);
+  const uint32_t xbytes = (uint32_t)TP * HW * (uint32_t)sizeof(T), dbytes = (uint32_t)TP * HWo * (uint32_t)sizeof(T);
   auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
   auto issue = [&](int n, int s) {
     if (lane == 0 && n < n1) {
       mbar_arrive_expect_tx(&bars[s], xbytes + dbytes);
       bulk_g2s(slot(s), x + ((int64_t)n * a.C + cb) * HW, xbytes, &bars[s]);
-      bulk_g2s(slot(s) + 4 * HW, dy + ((int64_t)n * a.C + cb) * HWo, dbytes, &bars[s]);
+      bulk_g2s(slot(s) + TP * HW, dy + ((int64_t)n * a.C + cb) * HWo, dbytes, &bars[s]);
     }
   };
   for (int i = 0; i < a.ns; ++i) issue(n0 + warp + i * nwarps, i);
   if (a.early_pdl) griddep_launch_dependents();  // grid is one wave: let the next kernel's CTAs queue
-  float run[9];
+  float run[NQ][9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) run[k] = 0.f;
+  for (int qd = 0; qd < NQ; ++qd)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) run[qd][k] = 0.f;
   int s = 0;
   uint32_t ph = 0;
   for (int n = n0 + warp; n < n1; n += nwarps) {
     mbar_wait(&bars[s], ph);
-    {  // every lane runs the loop (halo shuffles); only live lanes store / accumulate
-      const T* pln = slot(s) + pl * HW;
-      const T* pd = slot(s) + 4 * HW + pl * HWo;
+#pragma unroll
+    for (int qd = 0; qd < NQ; ++qd) {  // every lane runs the loop (halo shuffles); only live lanes accumulate
+      const T* pln = slot(s) + (qd * 4 + pl) * HW;
+      const T* pd = slot(s) + TP * HW + (qd * 4 + pl) * HWo;
       float xw[3][NXW];
 #pragma unroll
       for (int u = 0; u < NXW; ++u) xw[0][u] = 0.f;
@@ -862,7 +964,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
       }
       if (live) {
 #pragma unroll
-        for (int k = 0; k < 9; ++k) run[k] += loc[k];
+        for (int k = 0; k < 9; ++k) run[qd][k] += loc[k];
       }
     }
     __syncwarp();
@@ -871,22 +973,25 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
   }
   if (!a.early_pdl) griddep_launch_dependents();
   __syncthreads();
-  float* red = reinterpret_cast<float*>(smem + 64 * nwarps);
+  float* red = reinterpret_cast<float*>(smem + 64 * nwarps);  // [warp][lane][NQ*9]; the ring is idle now
   if (live) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) red[(warp * 32 + lane) * 9 + k] = run[k];
+    for (int qd = 0; qd < NQ; ++qd)
+#pragma unroll
+      for (int k = 0; k < 9; ++k) red[(warp * 32 + lane) * (NQ * 9) + qd * 9 + k] = run[qd][k];
   }
   __syncthreads();
   float* part = a.ws_part + (int64_t)sl * a.C * 9;
-  for (int e = threadIdx.x; e < 4 * 9; e += blockDim.x) {
-    const int p = e / 9, k = e - p * 9;
+  for (int e = threadIdx.x; e < TP * 9; e += blockDim.x) {
+    const int ch = e / 9, k = e - ch * 9;  // channel cb + ch = quad ch / 4, lane group ch % 4
+    const int qd = ch >> 2, p = ch & 3;
     float tot = 0.f;
     for (int wv = 0; wv < nwarps; ++wv) {
-      float v = red[(wv * 32 + p * 7) * 9 + k];
-      for (int l = 1; l < 7; ++l) v += red[(wv * 32 + p * 7 + l) * 9 + k];
+      float v = red[(wv * 32 + p * 7) * (NQ * 9) + qd * 9 + k];
+      for (int l = 1; l < 7; ++l) v += red[(wv * 32 + p * 7 + l) * (NQ * 9) + qd * 9 + k];
       tot = (wv == 0) ? v : tot + v;
     }
-    part[(int64_t)(cb + p) * 9 + k] = tot;
+    part[(int64_t)(cb + ch) * 9 + k] = tot;
   }
   __threadfence();
   __syncthreads();
@@ -894,7 +999,7 @@ __global__ void __launch_bounds__(256) small_bf2_kernel(const SArgs a) {
     const int ngrp = (a.nslices + 31) / 32;
     nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
                              a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
-                             (int64_t)cb * 9, 36, a.dw, &s_last);
+                             (int64_t)cb * 9, TP * 9, a.dw, &s_last);
   }
 }
 
@@ -1097,9 +1202,16 @@ SKernelFn pick(int pass, int W) {
   }
 }
 template <class T>
-SKernelFn pick2(int pass, int W) {  // stride 2: fwd and bwd_filter
+SKernelFn pick2(int pass, int W) {  // stride 2: fwd, bwd_data, bwd_filter
   if (pass == 0) return W == 14 ? small_fwd2_kernel<T, 14> : W == 28 ? small_fwd2_kernel<T, 28> : nullptr;
-  if (pass == 2) return W == 14 ? small_bf2_kernel<T, 14> : W == 28 ? small_bf2_kernel<T, 28> : nullptr;
+  if (pass == 1) {  // bf16 7x7 dy planes: 8-plane tasks (4 x 98 B is not a 16-B multiple)
+    if (W == 14) return sizeof(T) == 2 ? small_bd2_kernel<T, 14, 8> : small_bd2_kernel<T, 14, 4>;
+    return W == 28 ? small_bd2_kernel<T, 28> : nullptr;
+  }
+  if (pass == 2) {
+    if (W == 14) return sizeof(T) == 2 ? small_bf2_kernel<T, 14, 8> : small_bf2_kernel<T, 14, 4>;
+    return W == 28 ? small_bf2_kernel<T, 28> : nullptr;
+  }
   return nullptr;
 }
 SKernelFn pair_kernel_for(int pass, int W) {
@@ -1133,13 +1245,16 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   const int S = g.sh;
   if (g.sw != S || g.H != g.W) return false;
   if (S == 1 && g.W != 7 && g.W != 14 && g.W != 28) return false;
-  if (S == 2 && ((g.W != 14 && g.W != 28) || pass == 1 || pass == 3)) return false;  // s2: fwd, bwd_filter
+  if (S == 2 && ((g.W != 14 && g.W != 28) || pass == 3)) return false;  // s2: fwd, bwd_data, bwd_filter
   if (S != 1 && S != 2) return false;
   if (g.C % 4 != 0 || g.N < 1) return false;
   const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
   if (pair && (g.dtype != DWCONV_BF16 || S != 1 || pass > 2 || (g.N * g.C) % 8 != 0 || (pass == 2 && g.C % 8))) return false;
-  const int64_t task_bytes = (pair ? 8 : 4) * g.H * g.W * eb;
-  const int64_t dy_bytes = (pair ? 8 : 4) * g.Ho * g.Wo * eb;
+  // the staged planes: x (fwd, bwd_filter) or dy (bwd_data); stride-2 bf16 bwd_data on 14x14 takes
+  // 8 dy planes per task (4 x 7x7 bf16 is not a 16-B multiple)
+  const int tp = (pair || (S == 2 && (pass == 1 || pass == 2) && eb == 2 && g.W == 14)) ? 8 : 4;
+  const int64_t task_bytes = tp * (pass == 1 ? g.Ho * g.Wo : g.H * g.W) * eb;
+  const int64_t dy_bytes = tp * g.Ho * g.Wo * eb;
   if (task_bytes % 16 != 0 || (pass >= 2 && dy_bytes % 16 != 0)) return false;  // bulk copies: 16-B granules
   *p = SmallPlan{};
   static const int warps_env = env_int("DWCONV_SMALL_WARPS", 4, 1, 8);
@@ -1152,7 +1267,7 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   p->S = S;
   p->pair = pair;
   p->smem = 64 * p->warps + p->warps * p->ns * (int)p->slot_bytes;
-  if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * (pair ? 18 : 9) * 4);
+  if (bf) p->smem = std::max(p->smem, 64 * p->warps + p->warps * 32 * (tp == 8 ? 18 : 9) * 4);
   if (p->smem > smem_optin - 1024) return false;
   SKernelFn fn = pair ? pair_kernel_for(pass, (int)g.W) : kernel_for(g.dtype, pass, (int)g.W, S);
   if (!fn) return false;
@@ -1167,7 +1282,8 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   p->occ = occ;
   p->sms = num_sms;
   if (!bf) {
-    p->ntasks = g.N * g.C / (pair ? 8 : 4);
+    if ((g.N * g.C) % tp != 0) return false;
+    p->ntasks = g.N * g.C / tp;
     p->grid = (int)std::min<int64_t>((p->ntasks + p->warps - 1) / p->warps, (int64_t)occ * num_sms);
     if (slices > 0) {  // fwd / bwd_data: `slices` = tasks per warp (an even split: no partial last round)
       const int64_t g2 = (p->ntasks + (int64_t)p->warps * slices - 1) / ((int64_t)p->warps * slices);
@@ -1178,7 +1294,8 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
     return true;
   }
   // bwd_filter: groups of 4 (pair: 8) channels x batch slices, ~one wave, <= 32 images per warp
-  p->groups = (int)(g.C / (pair ? 8 : 4));
+  if (g.C % tp != 0) return false;
+  p->groups = (int)(g.C / tp);
   int64_t nsl = std::max<int64_t>(1, ((int64_t)occ * num_sms) / p->groups);
   nsl = std::max<int64_t>(nsl, (g.N + 32 * p->warps - 1) / (32 * p->warps));
   nsl = std::min<int64_t>(nsl, std::min<int64_t>(g.N, 128));
