@@ -165,6 +165,10 @@ struct NhwcGenPlan {
   int64_t tiles;
   int PS, nslices, rps, max_chain;            // bwd_filter
   size_t part_off, l2_off, t1_off, t2_off, ws_bytes;
+  // bwd_filter staged through shared memory by tensor-map TMA (tma = true)
+  bool tma;
+  int CB, NCP, NCS, CW, TR, XR, BWX, bpi, units, ups;
+  uint32_t x_bytes, dy_bytes, stage_bytes;
 };
 bool plan_nhwc_gen(const Geom& g, int pass, int num_sms, int smem_optin, NhwcGenPlan* plan);
 cudaError_t launch_nhwc_gen_fd(const Geom& g, const NhwcGenPlan& p, const void* in, const void* w, void* out,

@@ -32,6 +32,8 @@
 //    the last CTA of each group of 32 slices and then of the channel block sums the
 //    partials pairwise in slice order (integer tickets; nchw::finalize_two_level):
 //    no float atomics, bitwise reproducible, max_chain reported.
+#include <cuda.h>
+
 #include <algorithm>
 
 #include "kernels.h"
@@ -358,6 +360,220 @@ __global__ void __launch_bounds__(256, (M >= 4 ? 1 : 2)) gen_bf_kernel(const BAr
   griddep_launch_dependents();
 }
 
+// ---------------------------------------------------------------------------
+// bwd_filter, TMA-staged (the default where the tensors are 16-B aligned): CTA =
+// (block of CB channels = 64 B per pixel, slice of TR-row output bands).  A producer
+// lane stages each band's x rows [oh0*S-P, oh0*S-P+(TR-1)*S+K) x all columns (4-D
+// tensor-map box, zero-filled halo and tail) and its dy rows into a 2-stage ring;
+// consumer thread = (channel pair cp, column set cs, tap row i) walks its columns of
+// every band row with a K-wide sliding x window in registers read from shared memory
+// (S new pairs + M dy values per output pixel, K*M packed FFMA2).  Row sums (<= 64
+// terms) -> running sum over the slice's rows -> column sets in order -> slice
+// partial -> the two-level ticketed finalize (deterministic, no float atomics).
+struct TArgs {
+  float* dw;
+  float* part;
+  float* l2;
+  unsigned* t1;
+  unsigned* t2;
+  int C, Ho, Wo;
+  int CB, NCP, NCS, CW, TR, XR, BWX;
+  int ncb, bpi, units, nslices, ups;     // bands per image, band units, slices, units per slice
+  uint32_t x_bytes, dy_bytes, dy_off, stage_bytes;  // dy_off: x region rounded up to 128 B (TMA destination)
+};
+
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                     uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class T>
+__device__ __forceinline__ float2 ld_pair(const T* p) {
+  if constexpr (sizeof(T) == 4) {
+    return *reinterpret_cast<const float2*>(p);
+  } else {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+    return make_float2(nchw::bf_lo(w), nchw::bf_hi(w));
+  }
+}
+
+template <class T, int K, int S, int M>
+__global__ void __launch_bounds__(288) gen_bft_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                      const __grid_constant__ CUtensorMap tmd, const TArgs a) {
+  constexpr int P = (K - 1) / 2, NS = 2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_flag;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NS;
+  unsigned char* ring = smem + 128;
+  const int tid = threadIdx.x;
+  const int ncw = (blockDim.x - 32) >> 5;  // consumer warps
+  const int cb = blockIdx.x % a.ncb, sl = blockIdx.x / a.ncb;
+  const int u0 = sl * a.ups, u1 = min(a.units, u0 + a.ups);
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], ncw);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_wait();
+  const int ctid = tid - 32;
+  const int cp = ctid % a.NCP, rest = ctid / a.NCP;
+  const int cs = rest % a.NCS, i = rest / a.NCS;
+  const bool live = ctid >= 0 && i < K;
+  float2 run[K][M];
+#pragma unroll
+  for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+    for (int j = 0; j < M; ++j) run[jj][j] = make_float2(0.f, 0.f);
+  if (tid < 32) {
+    if (tid == 0) {  // producer
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = u0, it = 0; u < u1; ++u, ++it) {
+        if (it >= NS) mbar_wait(&empty[st], ph ^ 1);
+        const int n = u / a.bpi, oh0 = (u - n * a.bpi) * a.TR;
+        unsigned char* sx = ring + (size_t)st * a.stage_bytes;
+        mbar_arrive_expect_tx(&full[st], a.x_bytes + a.dy_bytes);
+        tma4(sx, &tmx, cb * a.CB, -P, oh0 * S - P, n, &full[st]);
+        tma4(sx + a.dy_off, &tmd, cb * a.CB * M, 0, oh0, n, &full[st]);
+        if (++st == NS) { st = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    int st = 0;
+    uint32_t ph = 0;
+    const int c_lo = cs * a.CW, c_hi = min(a.Wo, c_lo + a.CW);
+    for (int u = u0; u < u1; ++u) {
+      mbar_wait(&full[st], ph);
+      if (live) {
+        const int n = u / a.bpi, oh0 = (u - n * a.bpi) * a.TR;
+        const T* sx = reinterpret_cast<const T*>(ring + (size_t)st * a.stage_bytes);
+        const T* sd = reinterpret_cast<const T*>(ring + (size_t)st * a.stage_bytes + a.dy_off);
+        const int rows = min(a.TR, a.Ho - oh0);
+        for (int r = 0; r < rows; ++r) {
+          const T* xr = sx + ((size_t)(r * S + i) * a.BWX) * a.CB + 2 * cp;  // x row of tap row i
+          const T* dr = sd + ((size_t)r * a.Wo) * (a.CB * M) + 2 * cp * M;
+          float2 loc[K][M];
+#pragma unroll
+          for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+            for (int j = 0; j < M; ++j) loc[jj][j] = make_float2(0.f, 0.f);
+          float2 xw[K];
+#pragma unroll
+          for (int jj = 0; jj < K - S; ++jj) xw[jj] = ld_pair<T>(xr + (size_t)(c_lo * S + jj) * a.CB);
+          // unrolled so the window's register rotation costs moves only once per 8 pixels
+#pragma unroll 8
+          for (int ow = c_lo; ow < c_hi; ++ow) {
+#pragma unroll
+            for (int u2 = 0; u2 < S; ++u2) xw[K - S + u2] = ld_pair<T>(xr + (size_t)(ow * S + K - S + u2) * a.CB);
+            float dv[2 * M];  // dy[c0*M .. c0*M + 2M): channel c0 -> [0, M), c0+1 -> [M, 2M)
+#pragma unroll
+            for (int q = 0; q < M; ++q) {
+              const float2 v = ld_pair<T>(dr + (size_t)ow * (a.CB * M) + 2 * q);
+              dv[2 * q] = v.x;
+              dv[2 * q + 1] = v.y;
+            }
+#pragma unroll
+            for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+              for (int j = 0; j < M; ++j)
+                loc[jj][j] = __ffma2_rn(xw[jj], make_float2(dv[j], dv[M + j]), loc[jj][j]);
+#pragma unroll
+            for (int jj = 0; jj < K - S; ++jj) xw[jj] = xw[jj + S];
+          }
+#pragma unroll
+          for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+              run[jj][j].x += loc[jj][j].x;
+              run[jj][j].y += loc[jj][j].y;
+            }
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+      if (++st == NS) { st = 0; ph ^= 1; }
+    }
+  }
+  griddep_launch_dependents();
+  __syncthreads();  // the ring is idle: reuse it for the column-set reduction
+  float* red = reinterpret_cast<float*>(ring);  // [cs][cp][i][2][M][K]
+  const int per = 2 * M * K;
+  if (live) {
+    float* mine = red + ((size_t)(cs * a.NCP + cp) * K + i) * per;
+#pragma unroll
+    for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        mine[(0 * M + j) * K + jj] = run[jj][j].x;
+        mine[(1 * M + j) * K + jj] = run[jj][j].y;
+      }
+  }
+  __syncthreads();
+  const int64_t sstride = (int64_t)a.C * M * K * K;
+  if (live && cs == 0) {
+    float* dst = a.part + (int64_t)sl * sstride;
+    for (int e = 0; e < per; ++e) {
+      float v = red[((size_t)(0 * a.NCP + cp) * K + i) * per + e];
+      for (int c2 = 1; c2 < a.NCS; ++c2) v += red[((size_t)(c2 * a.NCP + cp) * K + i) * per + e];
+      const int h = e / (M * K), j = (e / K) % M, jj = e % K;
+      const int o = (cb * a.CB + 2 * cp + h) * M + j;
+      __stcg(dst + ((int64_t)o * K + i) * K + jj, v);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  const int64_t e0 = (int64_t)cb * a.CB * M * K * K;
+  nchw::finalize_two_level(a.part, a.l2, a.t1, a.t2, cb, sl, a.nslices, sstride, e0, a.CB * M * K * K, a.dw,
+                           &s_flag);
+}
+
+using BftFn = void (*)(const CUtensorMap, const CUtensorMap, const TArgs);
+template <class T, int K, int S>
+BftFn bft_m(int M) {
+  switch (M) {
+    case 1: return gen_bft_kernel<T, K, S, 1>;
+    case 2: return gen_bft_kernel<T, K, S, 2>;
+    case 4: return gen_bft_kernel<T, K, S, 4>;
+    default: return nullptr;
+  }
+}
+template <class T>
+BftFn bft_k(int K, int S, int M) {
+  if (S != 1 && S != 2) return nullptr;
+  switch (K) {
+    case 3: return S == 1 ? bft_m<T, 3, 1>(M) : bft_m<T, 3, 2>(M);
+    case 5: return S == 1 ? bft_m<T, 5, 1>(M) : bft_m<T, 5, 2>(M);
+    case 7: return S == 1 ? bft_m<T, 7, 1>(M) : bft_m<T, 7, 2>(M);
+    default: return nullptr;
+  }
+}
+BftFn bft_kernel(int dtype, int K, int S, int M) {
+  return dtype == DWCONV_F32 ? bft_k<float>(K, S, M) : bft_k<__nv_bfloat16>(K, S, M);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = []() -> EncodeFn {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<EncodeFn>(ptr);
+  }();
+  return fn;
+}
+
 using FdFn = void (*)(const FArgs);
 using BfFn = void (*)(const BArgs);
 
@@ -433,6 +649,66 @@ cudaError_t launch_ex(const void* fn, int grid, int block, int smem, cudaStream_
 
 }  // namespace nhwcg
 
+// the TMA-staged bwd_filter (gen_bft_kernel) where its boxes fit; false -> the direct kernel
+static bool plan_staged_bf(const Geom& g, int num_sms, int smem_optin, NhwcGenPlan* p) {
+  using namespace nhwcg;
+  const int K = g.kh, S = g.sh, M = g.m;
+  const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+  const int CB = 64 / eb;
+  if (g.C % CB != 0 || !bft_kernel(g.dtype, K, S, M) || !encode_fn()) return false;
+  const int64_t BWX = (g.Wo - 1) * S + K;
+  if (BWX > 256 || g.Wo > 256 || CB * M > 256 || g.N >= (1 << 24)) return false;
+  const int NCP = CB / 2;
+  int NCS = std::max(1, 256 / (NCP * K));
+  NCS = std::min<int>(NCS, (int)std::max<int64_t>(1, g.Wo / 4));
+  const int CW = (int)((g.Wo + NCS - 1) / NCS);
+  if (CW > 64) return false;
+  const int consumers = NCP * NCS * K;
+  const int threads = 32 + (consumers + 31) / 32 * 32;
+  if (threads > 288) return false;
+  int TR = 0;
+  uint32_t xb = 0, db = 0, stb = 0;
+  for (int tr : {4, 2, 1}) {
+    const int XR = (tr - 1) * S + K;
+    xb = (uint32_t)(XR * BWX * CB * eb);
+    db = (uint32_t)(tr * g.Wo * CB * M * eb);
+    stb = (((xb + 127) & ~127u) + db + 127) & ~127u;
+    const size_t red = (size_t)NCS * NCP * K * 2 * M * K * 4;
+    if (128 + 2 * (size_t)stb <= (size_t)std::min(smem_optin, 112 * 1024) && red <= 2 * (size_t)stb) {
+      TR = tr;
+      break;
+    }
+  }
+  if (TR == 0) return false;
+  p->tma = true;
+  p->CB = CB; p->NCP = NCP; p->NCS = NCS; p->CW = CW; p->TR = TR; p->XR = (TR - 1) * S + K; p->BWX = (int)BWX;
+  p->x_bytes = xb; p->dy_bytes = db; p->stage_bytes = stb;
+  p->ncb = (int)(g.C / CB);
+  p->bpi = (int)((g.Ho + TR - 1) / TR);
+  p->units = (int)(g.N * p->bpi);
+  p->threads = threads;
+  p->smem = 128 + 2 * (int)stb;
+  // about two waves of CTAs; each thread adds at most 48 row sums into its running sum
+  const int ups_max = std::max(1, 48 / TR);
+  int64_t ns = std::max<int64_t>(1, (int64_t)num_sms * 4 / p->ncb);
+  ns = std::max<int64_t>(ns, (p->units + ups_max - 1) / ups_max);
+  ns = std::min<int64_t>(ns, p->units);
+  p->ups = (int)((p->units + ns - 1) / ns);
+  p->nslices = (p->units + p->ups - 1) / p->ups;
+  p->grid = p->ncb * p->nslices;
+  const int64_t sstride = g.C * g.m * K * K;
+  const int ngrp = (p->nslices + 31) / 32;
+  int lg2 = 0;
+  while ((1 << lg2) < ngrp) ++lg2;
+  p->max_chain = CW + p->ups * TR + (NCS - 1) + 5 + lg2 + 1;
+  p->part_off = 0;
+  p->l2_off = (size_t)p->nslices * sstride * 4;
+  p->t1_off = p->l2_off + (size_t)ngrp * sstride * 4;
+  p->t2_off = p->t1_off + (size_t)p->ncb * ngrp * 4;
+  p->ws_bytes = (p->t2_off + (size_t)p->ncb * 4 + 15) & ~(size_t)15;
+  return p->max_chain <= 160;
+}
+
 bool plan_nhwc_gen(const Geom& g, int pass, int num_sms, int smem_optin, NhwcGenPlan* p) {
   using namespace nhwcg;
   if (g.layout != DWCONV_NHWC || g.kh != g.kw || g.sh != g.sw || g.ph != g.pw || g.ph != (g.kh - 1) / 2)
@@ -466,6 +742,7 @@ bool plan_nhwc_gen(const Geom& g, int pass, int num_sms, int smem_optin, NhwcGen
     return true;
   }
   if (pass != DWCONV_PASS_BWD_FILTER || !bf_kernel(g.dtype, K, S, M)) return false;
+  if (plan_staged_bf(g, num_sms, smem_optin, p)) return true;
   const int64_t rows = g.N * g.Ho;
   p->PS = std::max(1, 256 / (p->CVB * K));
   if (p->PS > 4) p->PS = 4;
@@ -519,6 +796,52 @@ cudaError_t launch_nhwc_gen_fd(const Geom& g, const NhwcGenPlan& p, const void* 
 cudaError_t launch_nhwc_gen_bf(const Geom& g, const NhwcGenPlan& p, const void* x, const void* dy, float* dw,
                                void* ws, cudaStream_t st) {
   using namespace nhwcg;
+  if (p.tma) {
+    BftFn fn = bft_kernel(g.dtype, p.K, p.S, p.M);
+    EncodeFn enc = encode_fn();
+    if (!fn || !enc) return cudaErrorNotSupported;
+    const int eb = g.dtype == DWCONV_F32 ? 4 : 2;
+    const CUtensorMapDataType dt = g.dtype == DWCONV_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap tmx, tmd;
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    {
+      const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+      const cuuint64_t str[3] = {(cuuint64_t)(g.C * eb), (cuuint64_t)(g.W * g.C * eb), (cuuint64_t)(g.H * g.W * g.C * eb)};
+      const cuuint32_t box[4] = {(cuuint32_t)p.CB, (cuuint32_t)p.BWX, (cuuint32_t)p.XR, 1};
+      if (enc(&tmx, dt, 4, const_cast<void*>(x), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    {
+      const int64_t Co = g.C * g.m;
+      const cuuint64_t dims[4] = {(cuuint64_t)Co, (cuuint64_t)g.Wo, (cuuint64_t)g.Ho, (cuuint64_t)g.N};
+      const cuuint64_t str[3] = {(cuuint64_t)(Co * eb), (cuuint64_t)(g.Wo * Co * eb), (cuuint64_t)(g.Ho * g.Wo * Co * eb)};
+      const cuuint32_t box[4] = {(cuuint32_t)(p.CB * g.m), (cuuint32_t)g.Wo, (cuuint32_t)p.TR, 1};
+      if (enc(&tmd, dt, 4, const_cast<void*>(dy), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    unsigned char* b = static_cast<unsigned char*>(ws);
+    TArgs a{};
+    a.dw = dw;
+    a.part = reinterpret_cast<float*>(b + p.part_off);
+    a.l2 = reinterpret_cast<float*>(b + p.l2_off);
+    a.t1 = reinterpret_cast<unsigned*>(b + p.t1_off);
+    a.t2 = reinterpret_cast<unsigned*>(b + p.t2_off);
+    a.C = (int)g.C; a.Ho = (int)g.Ho; a.Wo = (int)g.Wo;
+    a.CB = p.CB; a.NCP = p.NCP; a.NCS = p.NCS; a.CW = p.CW; a.TR = p.TR; a.XR = p.XR; a.BWX = p.BWX;
+    a.ncb = p.ncb; a.bpi = p.bpi; a.units = p.units; a.nslices = p.nslices; a.ups = p.ups;
+    a.x_bytes = p.x_bytes; a.dy_bytes = p.dy_bytes; a.stage_bytes = p.stage_bytes;
+    a.dy_off = (p.x_bytes + 127) & ~127u;
+    if (p.smem > 48 * 1024 &&
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             p.smem) != cudaSuccess)
+      return cudaErrorInvalidValue;
+    void* args[] = {&tmx, &tmd, &a};
+    return launch_ex(reinterpret_cast<const void*>(fn), p.grid, p.threads, p.smem, st, args);
+  }
   BfFn fn = bf_kernel(g.dtype, p.K, p.S, p.M);
   if (!fn) return cudaErrorNotSupported;
   unsigned char* b = static_cast<unsigned char*>(ws);

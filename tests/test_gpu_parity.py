@@ -423,6 +423,12 @@ NHWC_GEN_SHAPES = [
     (2, 4, 12, 12, 2, 5, 2, 2),
     (3, 8, 7, 9, 4, 3, 2, 1),
     (2, 4, 8, 8, 2, 7, 1, 3),
+    # channel counts that take the TMA-staged bwd_filter (C % 16 fp32 / % 32 bf16), ragged bands and columns
+    (2, 32, 13, 11, 2, 3, 1, 1),
+    (2, 64, 15, 17, 1, 5, 1, 2),
+    (1, 32, 14, 13, 1, 7, 2, 3),
+    (3, 64, 9, 10, 4, 3, 2, 1),
+    (1, 96, 30, 29, 1, 7, 1, 3),
 ]
 
 
