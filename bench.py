@@ -477,8 +477,10 @@ class Workload:
             mean_ms = e_a.elapsed_time(e_b) / (reps * nl)
             del g, sets
             nbytes = pass_bytes(L, pas, self.eb)
+            info = self.plans[li][pas].describe()
             kt.append(dict(layer=L.name, pass_=pas, ms=mean_ms, bytes=nbytes, gbs=nbytes / (mean_ms * 1e-3) / 1e9,
-                           li=li))
+                           li=li, variant=info["variant_name"], grid=info["grid"], block=info["block"],
+                           shape=f"{L.c}x{L.h}x{L.w}/s{L.s}"))
         return kt
 
     def step_bytes(self):

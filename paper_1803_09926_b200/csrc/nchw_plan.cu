@@ -135,6 +135,8 @@ int est_ctas_per_sm(int smem_bytes, int threads) {
 // Score of a candidate chunking: fraction of issued thread-strip slots doing real
 // work, discounted when chunks are tiny (per-chunk fixed costs) or the SM holds
 // too few warps to hide shared-memory latency.
+inline int64_t nps_guard(int64_t v) { return v < 1 ? 1 : v; }
+
 double chunk_score(int64_t useful, int64_t slots, int64_t chunk_bytes, int smem, int threads) {
   static const double min_chunk = 1024.0 * nchw::env_int("DWCONV_MIN_CHUNK_KB", 32, 1, 64);
   static const double occ_warps = nchw::env_int("DWCONV_OCC_WARPS", 16, 4, 64);
@@ -340,7 +342,10 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       // bytes in flight per SM: every resident CTA keeps its ring of input stages loading
       static const double fill_b = 1024.0 * env_int("DWCONV_FILL_KB", 160, 8, 228);
       const double fill_f = std::min(1.0, ctas_eff * c.ns * (double)c.in_bytes / fill_b);
-      const double sc = eff * pipe * occ_f * size_f * fill_f;
+      // SMs that get a chunk at all: tiny planes (4x4 .. 8x8, the width/resolution variants of
+      // configs[2]) otherwise pick a few huge chunks (measured: 43 CTAs, 44 us for a 2 MB pass)
+      const double sm_f = std::min(1.0, (double)nch / num_sms);
+      const double sc = eff * pipe * occ_f * size_f * fill_f * sm_f;
       keep(sc, c);
       if (sc > best) { best = sc; bestp = c; }
     };
@@ -524,6 +529,35 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
   const bool ok = finalize(p);
   if (cands) {
     collect_candidates(pool, ok ? p : nullptr, finalize, cands, max_cands);
+    // fewer batch slices for the leading shapes: on small tensors (the width/resolution
+    // variants of configs[2]: 1-2 MB per pass) one wave of CTAs leaves each with a few KB
+    // and the cross-slice finalize dominates; the measured selection decides
+    const size_t lead = std::min<size_t>(cands->size(), 4);
+    for (size_t ci = 0; ci < lead; ++ci) {
+      for (int div : {2, 4, 8}) {
+        ChunkPlan v = (*cands)[ci];
+        if (v.direct || v.small || v.nslices < 2 * div) continue;
+        const int64_t N = std::max<int64_t>(g.N, 1);
+        int64_t nsl = v.nslices / div;
+        int64_t nps = (N + nsl - 1) / nps_guard(nsl);
+        nsl = (N + nps - 1) / nps;
+        if (nps * v.nbands > 32) continue;  // running-sum chain, as finalize()
+        const int64_t old_nps = v.n_per_slice, old_nsl = v.nslices;
+        v.nslices = (int)nsl;
+        v.n_per_slice = (int)nps;
+        v.grid = (int)(v.groups * nsl);
+        v.nchunks = v.grid;
+        v.max_chain = v.max_chain - (int)(old_nps * v.nbands) + (int)(nps * v.nbands) -
+                      2 * ilog2_ceil(old_nsl) + 2 * ilog2_ceil(nsl);
+        v.ws_bytes = two_level_ws_bytes(v.groups, nsl, g.C * m, KK);
+        if (v.max_chain > 160 || (int)cands->size() >= max_cands) continue;
+        bool dup = false;
+        for (const ChunkPlan& o : *cands) dup = dup || (o.P == v.P && o.tpg == v.tpg && o.nbands == v.nbands &&
+                                                        o.band_rows == v.band_rows && o.nslices == v.nslices &&
+                                                        o.threads == v.threads && o.direct == v.direct);
+        if (!dup) cands->push_back(v);
+      }
+    }
     if (!fused) {  // register-direct variants (no smem staging) compete too
       for (int tasks : {2, 4}) {
         ChunkPlan d;
