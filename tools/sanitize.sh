@@ -7,7 +7,7 @@ mkdir -p $out
 CS=/usr/local/cuda/bin/compute-sanitizer
 timeout 900 $CS --tool memcheck --leak-check no --error-exitcode 9 python tools/sanitize_cases.py --all-candidates \
   > $out/memcheck.log 2>&1; echo "memcheck rc=$?" >> $out/memcheck.log
-for c in cfg1 small14 small7_bf16 band112 band56_s2 nhwc_tma_s1 nhwc_tma_s2_bf16 k5 k7_nhwc m2 bdmma_k5; do
+for c in cfg1 small14 small7_bf16 band56_s2 nhwc_tma_s1 nhwc_tma_s2_bf16 k5 k7_nhwc m2 bdmma_k5 small14_s2 small14_s2_bf16 nhwc_gen_k5; do
   timeout 600 $CS --tool racecheck --racecheck-report all --print-limit 100000000 python tools/sanitize_cases.py --all-candidates --only $c \
     2>&1 | python tools/racecheck_summary.py > $out/racecheck_$c.txt
 done

@@ -31,6 +31,9 @@ CASES = [  # name, (N, C, H, W, m, K, s, p), layout, dtype
     ("k7_nhwc", (2, 32, 28, 28, 1, 7, 1, 3), NHWC, "bf16"),
     ("m2", (2, 16, 28, 28, 2, 3, 1, 1), NHWC, "f32"),
     ("bdmma_k5", (2, 64, 20, 20, 1, 5, 1, 2), NHWC, "bf16"),  # tcgen05 block-diagonal candidates
+    ("small14_s2", (4, 32, 14, 14, 1, 3, 2, 1), NCHW, "f32"),  # stride-2 small-plane fwd / bwd_data / bwd_filter
+    ("small14_s2_bf16", (2, 64, 14, 14, 1, 3, 2, 1), NCHW, "bf16"),  # 8-plane tasks / 8-channel groups
+    ("nhwc_gen_k5", (2, 64, 20, 20, 1, 5, 1, 2), NHWC, "f32"),  # NHWC general kernels, TMA-staged bwd_filter
 ]
 
 
