@@ -143,9 +143,10 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzled stages (the host adds 1 KB of slack)
   unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  unsigned char* stages = smem;
-  unsigned char* bw = smem + NS * a.stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bw + a.bw_bytes);
+  // [barriers + TMEM slot: 1 KB][stages (1024-B aligned)][diagonal weight tiles]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  unsigned char* stages = smem + 1024;
+  unsigned char* bw = stages + NS * a.stage_bytes;
   uint64_t* full = bars;
   uint64_t* empty = bars + NS;
   uint64_t* tfull = bars + 2 * NS;
@@ -167,7 +168,8 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
     }
     fence_mbar_init();
   }
-  if (warp == 1) {
+  __syncthreads();  // barrier inits visible before any other shared-memory traffic (TMEM alloc included)
+  if (warp == 3) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tbase_slot)),
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) bdmma_kernel(const __grid_constan
   tc_fence_before();
   __syncthreads();
   griddep_launch_dependents();
-  if (warp == 1) {
+  if (warp == 3) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
   }
@@ -355,7 +357,9 @@ int th_of(int CB) { return 512 / CB; }
 int smem_bytes(int K, int S, int CB) {
   const int BH = th_of(CB) + K - 1;
   const int nacc = 2 * (th_of(CB) * BW / 128);
-  return 1024 + NS * (BH + 1) * BW * CB * 2 + K * K * (CB / S) * S * S * 2 + (2 * NS + 2 * nacc) * 8 + 16;
+  static_assert((2 * NS + 2 * 16) * 8 + 16 <= 1024, "barriers fit the 1 KB header");
+  (void)nacc;
+  return 1024 + 1024 + NS * (BH + 1) * BW * CB * 2 + K * K * (CB / S) * S * S * 2;
 }
 
 }  // namespace bdmma
