@@ -37,7 +37,7 @@ CASES = [  # name, (N, C, H, W, m, K, s, p), layout, dtype
 ]
 
 
-def run(name, shp, layout, dtype, all_cands):
+def run(name, shp, layout, dtype, all_cands, skip=()):
     N, C, H, W, m, K, s, p = shp
     d = ops.make_desc(N, C, H, W, m, K, s, p, layout, F32 if dtype == "f32" else BF16)
     Ho, Wo = ops.output_shape(d)
@@ -51,7 +51,7 @@ def run(name, shp, layout, dtype, all_cands):
     dw = torch.empty(C * m, K, K, device="cuda")
     for pas in (0, 1, 2):
         cands = ops.dwconv_plan_candidates(d, pas) if all_cands else []
-        idxs = list(range(len(cands))) or [None]
+        idxs = [i for i in range(len(cands)) if cands[i]["variant_name"] not in skip] or [None]
         ws = torch.zeros(max([16, ops.dwconv_bwd_filter_workspace_bytes(d)] +
                              [c["workspace_bytes"] for c in cands]), dtype=torch.uint8, device="cuda")
         for i in idxs:
@@ -76,7 +76,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--all-candidates", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--skip-variant", default="", help="comma list of candidate variants not to launch")
     a = ap.parse_args()
     for c in CASES:
         if not a.only or c[0] in a.only.split(","):
-            run(*c, a.all_candidates)
+            run(*c, a.all_candidates, tuple(v for v in a.skip_variant.split(",") if v))
