@@ -175,6 +175,10 @@ typedef struct {
   int32_t batch_slices;       /* bwd_filter: CTAs that share one channel group              */
   int32_t max_chain;          /* bwd_filter: worst-case serial-add depth of any dw element  */
   int64_t workspace_bytes;    /* bwd_filter workspace                                       */
+  int32_t kernel_family;      /* NCHW chunk variant: 0 warp-specialised chunk, 1 small-plane
+                                 warp tasks, 2 band bwd_filter, 3 register-direct bwd_filter,
+                                 4 streaming bf16 bwd_filter; 0 for other variants          */
+  int32_t reserved;
 } dwconv_plan_info;
 DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info);
 
@@ -199,7 +203,7 @@ DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* inf
  *     dwconv_plan_select changes process-wide behaviour for every later call with
  *     that descriptor; callers that must not see (or make) such changes use the
  *     immutable plan handles below (what tune.py and bench.py do). */
-#define DWCONV_MAX_CANDIDATES 32
+#define DWCONV_MAX_CANDIDATES 48
 DWCONV_API int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, dwconv_plan_info* infos,
                                       int* count);
 DWCONV_API int dwconv_plan_select(const dwconv_desc* d, int pass, int index);

@@ -22,7 +22,7 @@ FUNCTIONS = ("dwconv_abi_version", "dwconv_status_string", "dwconv_output_shape"
              "dwconv_set_variant_override", "dwconv_plan_create", "dwconv_plan_destroy", "dwconv_plan_describe",
              "dwconv_plan_workspace_bytes", "dwconv_fwd_plan", "dwconv_bwd_data_plan", "dwconv_bwd_filter_plan",
              "dwconv_bwd_plan")
-MAX_CANDIDATES = 32
+MAX_CANDIDATES = 48
 
 
 class Desc(ctypes.Structure):
@@ -38,7 +38,8 @@ class PlanInfo(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int32), ("launches", ctypes.c_int32), ("work_units", ctypes.c_int64),
                 ("planes_per_chunk", ctypes.c_int32), ("rows_per_band", ctypes.c_int32),
                 ("batch_slices", ctypes.c_int32), ("max_chain", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_int64), ("kernel_family", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class DwconvError(RuntimeError):

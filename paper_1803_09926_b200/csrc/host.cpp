@@ -469,6 +469,7 @@ static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* 
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
     info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
     info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
+    info->kernel_family = c.direct ? (c.dstream > 0 ? 4 : 3) : (c.small ? (c.sp.band ? 2 : 1) : 0);
   } else if (p.variant == DWCONV_VARIANT_NHWC_TMA) {
     const dwk::NhwcTmaPlan& c = p.tma;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
@@ -657,7 +658,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         for (const ChunkPlan& o : cands)
           dup = dup || (o.P == c.P && o.nbands == c.nbands && o.band_rows == c.band_rows && o.threads == c.threads &&
                         o.tpg == c.tpg && o.ns == c.ns && o.pair == c.pair && o.direct == c.direct &&
-                        o.small == c.small && o.sp.band == c.sp.band && o.sp.ppw == c.sp.ppw && o.nslices == c.nslices &&
+                        o.dstream == c.dstream && o.V == c.V && o.small == c.small && o.sp.band == c.sp.band && o.sp.ppw == c.sp.ppw && o.nslices == c.nslices &&
                         o.grid == c.grid);
         if (!dup) cands.push_back(c);
       }

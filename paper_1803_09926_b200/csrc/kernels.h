@@ -92,6 +92,7 @@ struct ChunkPlan {
   // bwd_filter register-direct variant (direct_bwd_filter.cu): no smem staging
   bool direct;
   int dL, dSPW, dspc;   // lanes per row set, row sets per warp, row sets per channel
+  int dstream;          // > 0: bf16 streaming variant (sdbf_kernel) with bands of dstream dy rows
   // small-plane warp-task kernels (nchw_small.cu)
   bool small;
   SmallPlan sp;

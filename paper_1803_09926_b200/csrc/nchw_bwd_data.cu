@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
   constexpr int TW = (S == 1) ? V : S * V;  // dx columns per thread tile (stride aligned)
   constexpr int NCY = floor_div(TW - 1 + PAD, S) - D0 + 1;
   static_assert(R % S == 0, "dx strip must be stride aligned");
+  // bf16 3x3 stride 2, m = 1: streaming polyphase strip (see below)
+  constexpr bool kStream = std::is_same<T, __nv_bfloat16>::value && K == 3 && S == 2 && V >= 2 && kBf16Interleave;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 64);
@@ -237,6 +239,77 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
         const int sb = t2 - pp * a.nsb;
         const int ih0 = k.r0 + sb * R;  // multiple of S
         const int iw0 = cb * TW;
+        if constexpr (kStream) {
+          if (m == 1) {
+            // dx rows stream down the strip: even dx row ih0+2s takes dy row a0+s (tap row 1), odd
+            // row ih0+2s+1 takes dy rows a0+s (tap row 2) and a0+s+1 (tap row 0); columns alike
+            // (dx column iw0+2b: dy column c0+b, tap 1; iw0+2b+1: c0+b+1, tap 0 and c0+b, tap 2).
+            // FFMA2 lanes = dx columns (u, u+V), so the operand pairs are P[k] = (dy[c0+k], dy[c0+k+V/2]),
+            // widened once per dy row (nchw_common.cuh interleaved pairs); 2 dy rows live.
+            float wr[KK];
+            if (ww.tma) {
+#pragma unroll
+              for (int q = 0; q < KK; ++q) wr[q] = Elem<T>::load(swr + pp * KK + q);
+            } else {
+#pragma unroll
+              for (int q = 0; q < KK; ++q) wr[q] = swc[pp * KK + q];
+            }
+            const int a0 = ih0 / 2, c0 = iw0 / 2;
+            const T* splane = sin + pp * sp.pitch + sp.zbe - k.lo * Wo;  // dy row oh at splane + oh * Wo
+            const bool hok = c0 + V < Wo;
+            auto load_pairs = [&](int oh, float2* P) {
+              const bool rok = PADDED || (unsigned)(oh - k.lo) < (unsigned)rows_dy;
+              const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>((rok ? splane + oh * Wo : zrow) + c0);
+              uint32_t wv[V / 2];
+              load_words<V / 2>(p, wv);
+              const uint32_t h = hok ? (uint32_t)reinterpret_cast<const unsigned short*>(p)[V] : 0u;
+              auto val = [&](int q) -> float { return q < V ? ((q & 1) ? bfw_hi(wv[q >> 1]) : bfw_lo(wv[q >> 1])) : bfw_lo(h); };
+#pragma unroll
+              for (int kk = 0; kk <= V / 2; ++kk) P[kk] = make_float2(val(kk), val(kk + V / 2));
+            };
+            auto put_row = [&](int ih, const float2* e) {
+              if (ih >= k.r1) return;
+              float v[TW];
+#pragma unroll
+              for (int u = 0; u < V; ++u) { v[u] = e[u].x; v[u + V] = e[u].y; }
+              T* row = dx + (k.q0 + pp) * (int64_t)H * W + (int64_t)ih * W + iw0;
+              if (W % TW == 0) {
+                VecIO<T, TW>::store(row, v);
+              } else {
+#pragma unroll
+                for (int u = 0; u < TW; ++u)
+                  if (iw0 + u < W) Elem<T>::store(row + u, v[u]);
+              }
+            };
+            auto f2 = [](float w) { return make_float2(w, w); };
+            float2 Pc[V / 2 + 1], Pn[V / 2 + 1];
+            load_pairs(a0, Pc);
+#pragma unroll
+            for (int s2 = 0; s2 < R / 2; ++s2) {
+              float2 e[V];
+#pragma unroll
+              for (int b = 0; b < V / 2; ++b) {
+                e[2 * b] = __fmul2_rn(f2(wr[4]), Pc[b]);
+                e[2 * b + 1] = __ffma2_rn(f2(wr[5]), Pc[b], __fmul2_rn(f2(wr[3]), Pc[b + 1]));
+              }
+              put_row(ih0 + 2 * s2, e);
+              load_pairs(a0 + s2 + 1, Pn);
+#pragma unroll
+              for (int b = 0; b < V / 2; ++b) {
+                e[2 * b] = __ffma2_rn(f2(wr[7]), Pc[b], __fmul2_rn(f2(wr[1]), Pn[b]));
+                float2 o = __fmul2_rn(f2(wr[0]), Pn[b + 1]);
+                o = __ffma2_rn(f2(wr[2]), Pn[b], o);
+                o = __ffma2_rn(f2(wr[6]), Pc[b + 1], o);
+                e[2 * b + 1] = __ffma2_rn(f2(wr[8]), Pc[b], o);
+              }
+              put_row(ih0 + 2 * s2 + 1, e);
+#pragma unroll
+              for (int kk = 0; kk <= V / 2; ++kk) Pc[kk] = Pn[kk];
+            }
+            continue;
+          }
+        }
+        if constexpr (!(kStream && V >= 8)) {
         float acc[R][TW];
 #pragma unroll
         for (int tt = 0; tt < R; ++tt)
@@ -324,6 +397,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
             }
           }
         }
+        }
       }
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
@@ -360,6 +434,10 @@ KernelFn pick_rv(int RI, int VI) {
       case 1: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 2, PD> : nchw_bwd_data_kernel<T, K, S, R1, 2, PD>;
       case 2:
         if constexpr (K == 3) return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 4, PD> : nchw_bwd_data_kernel<T, K, S, R1, 4, PD>;
+        else return nullptr;
+      case 3:  // bf16 3x3 streaming strips (m = 1), 16 dx columns
+        if constexpr (K == 3 && PD && std::is_same<T, __nv_bfloat16>::value)
+          return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 8, PD> : nchw_bwd_data_kernel<T, K, S, R1, 8, PD>;
         else return nullptr;
       default: return nullptr;
     }

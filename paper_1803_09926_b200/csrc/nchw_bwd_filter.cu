@@ -26,7 +26,9 @@ template <class T, int K, int S, int R, int V, bool PADDED, bool FUSED = false>
 __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int NRows = (R - 1) * S + K;
-  constexpr bool kPacked = (S == 1 && V % 2 == 0);  // float2 accumulators, FFMA2
+  // bf16, V >= 4: interleaved pairs (lanes = columns u, u + V/2; nchw_common.cuh), FFMA2 at any stride
+  constexpr bool kIl = std::is_same<T, __nv_bfloat16>::value && V >= 4 && kBf16Interleave;
+  constexpr bool kPacked = kIl || (S == 1 && V % 2 == 0);  // float2 accumulators, FFMA2
   using Wd = Win<K, S, V>;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -165,6 +167,47 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
         const int sb = (int)fdiv((uint32_t)t, a.div_ncg);
         const int c0 = (t - sb * ncg) * V;
         const int oh0 = r.r0 + sb * R;
+        const int b0 = S * c0;
+        bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+        for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
+#pragma unroll
+        for (int q = 0; q < Wd::NR; ++q) rok[q] = b0 + Wd::NV + q < W;
+        const int ih0 = oh0 * S - PAD;
+        if constexpr (kIl) {
+          // dy row tt is loaded at its first use (input row tt*S): at most K/S + 1 rows live
+          float2 dv2[R][V / 2];
+#pragma unroll
+          for (int rr = 0; rr < NRows; ++rr) {
+#pragma unroll
+            for (int tt = 0; tt < R; ++tt) {
+              if (rr == tt * S) {
+                if (oh0 + tt < r.r1) {
+                  load_vec_bf2<V>(reinterpret_cast<const __nv_bfloat16*>(s_dy + (oh0 + tt) * Wo + c0), dv2[tt]);
+                } else {
+#pragma unroll
+                  for (int u = 0; u < V / 2; ++u) dv2[tt][u] = make_float2(0.f, 0.f);
+                }
+              }
+            }
+            const int ih = ih0 + rr;
+            const bool rv = PADDED || (unsigned)(ih - r.lo) < (unsigned)rows_x;
+            const T* p = (rv ? s_x + ih * W : zrow) + b0;
+            float2 X2[Win2<K, S, V>::NP];
+            load_window_bf2<K, S, V>(reinterpret_cast<const __nv_bfloat16*>(p), lok, rok, X2);
+#pragma unroll
+            for (int tt = 0; tt < R; ++tt) {
+              const int i = rr - tt * S;
+              if (i >= 0 && i < K) {
+#pragma unroll
+                for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+                  for (int u = 0; u < V / 2; ++u)
+                    loc2[i * K + jj] = __ffma2_rn(X2[S * u + jj], dv2[tt][u], loc2[i * K + jj]);
+              }
+            }
+          }
+        } else {
         float dv[R][V];
 #pragma unroll
         for (int tt = 0; tt < R; ++tt) {
@@ -175,13 +218,6 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
             for (int u = 0; u < V; ++u) dv[tt][u] = 0.f;
           }
         }
-        const int b0 = S * c0;
-        bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
-#pragma unroll
-        for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
-#pragma unroll
-        for (int q = 0; q < Wd::NR; ++q) rok[q] = b0 + Wd::NV + q < W;
-        const int ih0 = oh0 * S - PAD;
 #pragma unroll
         for (int rr = 0; rr < NRows; ++rr) {
           const int ih = ih0 + rr;
@@ -207,6 +243,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
               }
             }
           }
+        }
         }
         if constexpr (FUSED) {  // dx strip at the same rows / columns (S = 1: H = Ho, W = Wo)
           float acc[R][V];

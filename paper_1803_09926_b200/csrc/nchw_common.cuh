@@ -326,6 +326,135 @@ __device__ __forceinline__ WeightWin weight_win(const NArgs& a, int64_t q0, int 
   return r;
 }
 
+// ------------------------------------------------------------------ bf16 interleaved windows
+#ifndef DWCONV_BF16_IL
+#define DWCONV_BF16_IL 1
+#endif
+constexpr bool kBf16Interleave = DWCONV_BF16_IL != 0;
+template <int NW>
+__device__ __forceinline__ void load_words(const __nv_bfloat16* p, uint32_t* w) {
+  if constexpr (NW == 1) {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else if constexpr (NW == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    w[0] = v.x; w[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < NW / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[q];
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  }
+}
+// bf16 strips of V >= 4 columns pair output column u with column u + V/2 in one
+// FFMA2 (lanes = (u, u + V/2)), so the operand pair of tap jj is
+//   X2[S*u + jj] = (xw[S*u + jj], xw[S*u + jj + S*V/2]),
+// two window elements half a strip apart.  Every element has to be widened from
+// bf16 anyway, so each pair half is widened straight into its register: no
+// pair-forming moves (a (u, u+1) pairing needs them for every other tap, and
+// they issue as IMAD.MOV on the FMA pipe this path is bound by), at any stride.
+// The widening is PRMT / LOP3 (ALU pipe), kept out of IMAD by inline PTX.
+__device__ __forceinline__ float bfw_lo(uint32_t w) {  // low bf16 of a word -> fp32 (exact)
+  float r;
+  asm volatile("prmt.b32 %0, %1, 0, 0x1054;" : "=f"(r) : "r"(w));
+  return r;
+}
+__device__ __forceinline__ float bfw_hi(uint32_t w) {  // high bf16 of a word -> fp32 (exact)
+  float r;
+  asm volatile("and.b32 %0, %1, 0xffff0000;" : "=f"(r) : "r"(w));
+  return r;
+}
+template <int K, int S, int V>
+struct Win2 {
+  static_assert(V >= 4 && V % 2 == 0, "interleaved pairs need V >= 4");
+  static constexpr int H = S * V / 2;            // lane distance inside the window
+  static constexpr int NP = S * (V / 2 - 1) + K;  // operand pairs per row
+};
+// Window of one row (as Win<K,S,V>) in interleaved pairs X2[k] = (xw[k], xw[k + H]).
+template <int K, int S, int V>
+__device__ __forceinline__ void load_window_bf2(const __nv_bfloat16* p /* at column S*c0 */, const bool* lok,
+                                                const bool* rok, float2* X2) {
+  using Wd = Win<K, S, V>;
+  using W2 = Win2<K, S, V>;
+  static_assert(Wd::NV % 2 == 0, "whole 32-bit words");
+  constexpr int NW = Wd::NV / 2;
+  uint32_t wv[NW];
+  load_words<NW>(p, wv);
+  const unsigned short* us = reinterpret_cast<const unsigned short*>(p);
+  uint32_t hl[Wd::NL > 0 ? Wd::NL : 1], hr[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l) hl[l] = lok[l] ? (uint32_t)us[l - Wd::NL] : 0u;
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r) hr[r] = rok[r] ? (uint32_t)us[Wd::NV + r] : 0u;
+  auto val = [&](int k) -> float {  // xw[k]; k is a compile-time constant after unrolling
+    if (k < Wd::NL) return bfw_lo(hl[k]);
+    if (k < Wd::NL + Wd::NV) {
+      const int q = k - Wd::NL;
+      return (q & 1) ? bfw_hi(wv[q >> 1]) : bfw_lo(wv[q >> 1]);
+    }
+    return bfw_lo(hr[k - Wd::NL - Wd::NV]);
+  };
+#pragma unroll
+  for (int k = 0; k < W2::NP; ++k) X2[k] = make_float2(val(k), val(k + W2::H));
+}
+// V bf16 values at p (16-B / 8-B aligned) as pairs D2[u] = (v[u], v[u + V/2]).
+template <int V>
+__device__ __forceinline__ void load_vec_bf2(const __nv_bfloat16* p, float2* D2) {
+  uint32_t wv[V / 2];
+  load_words<V / 2>(p, wv);
+  auto val = [&](int q) -> float { return (q & 1) ? bfw_hi(wv[q >> 1]) : bfw_lo(wv[q >> 1]); };
+#pragma unroll
+  for (int u = 0; u < V / 2; ++u) D2[u] = make_float2(val(u), val(u + V / 2));
+}
+// The bf16 interleaved strip: same sums as stencil_strip (below), FFMA2 at any stride.
+template <int K, int S, int R, int V, bool PADDED>
+__device__ __forceinline__ void stencil_strip_bf2(const __nv_bfloat16* sp, const __nv_bfloat16* zp, int W, int lo,
+                                                  int rows, int ih0, int c0, const float* wr, float (&acc)[R][V]) {
+  using Wd = Win<K, S, V>;
+  using W2 = Win2<K, S, V>;
+  constexpr int NRows = (R - 1) * S + K;
+  const int b0 = S * c0;
+  bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r) rok[r] = b0 + Wd::NV + r < W;
+  float2 acc2[R][V / 2];
+#pragma unroll
+  for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+    for (int u = 0; u < V / 2; ++u) acc2[tt][u] = make_float2(acc[tt][u], acc[tt][u + V / 2]);
+  const __nv_bfloat16* prow = sp + ih0 * W + b0;
+#pragma unroll
+  for (int r = 0; r < NRows; ++r) {
+    const __nv_bfloat16* p;
+    if constexpr (PADDED) {
+      p = prow + r * W;
+    } else {
+      const bool rv = (unsigned)(ih0 + r - lo) < (unsigned)rows;
+      p = rv ? prow + r * W : zp + b0;
+    }
+    float2 X2[W2::NP];
+    load_window_bf2<K, S, V>(p, lok, rok, X2);
+#pragma unroll
+    for (int tt = 0; tt < R; ++tt) {
+      const int i = r - tt * S;
+      if (i >= 0 && i < K) {
+#pragma unroll
+        for (int jj = 0; jj < K; ++jj) {
+          const float w = wr[i * K + jj];
+#pragma unroll
+          for (int u = 0; u < V / 2; ++u) acc2[tt][u] = __ffma2_rn(make_float2(w, w), X2[S * u + jj], acc2[tt][u]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+    for (int u = 0; u < V / 2; ++u) { acc[tt][u] = acc2[tt][u].x; acc[tt][u + V / 2] = acc2[tt][u].y; }
+}
+
 // ------------------------------------------------------------------ stencil strip
 // acc[tt][u] = sum_{i,jj} wr[i*K+jj] * X[oh0*S - PAD + tt*S + i][S*(c0+u) - PAD + jj]
 // where input row ih lives at sp + ih*W.  PADDED: every row the strip touches is
@@ -335,6 +464,12 @@ __device__ __forceinline__ WeightWin weight_win(const NArgs& a, int64_t q0, int 
 template <class T, int K, int S, int R, int V, bool PADDED>
 __device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, int lo, int rows, int ih0, int c0,
                                               const float* wr, float (&acc)[R][V]) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value && V >= 4 && (S * V) % 2 == 0) {
+    if (kBf16Interleave) {
+      stencil_strip_bf2<K, S, R, V, PADDED>(sp, zp, W, lo, rows, ih0, c0, wr, acc);
+      return;
+    }
+  }
   using Wd = Win<K, S, V>;
   constexpr int NRows = (R - 1) * S + K;
   const int b0 = S * c0;
@@ -389,21 +524,6 @@ __device__ __forceinline__ void stencil_strip(const T* sp, const T* zp, int W, i
 // stride.  Window: columns [S*c0 - PAD, S*c0 - PAD + (V-1)*S + K), as Win<K,S,V>.
 __device__ __forceinline__ float bf_bits_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_bits_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-template <int NW>
-__device__ __forceinline__ void load_words(const __nv_bfloat16* p, uint32_t* w) {
-  if constexpr (NW == 1) {
-    w[0] = *reinterpret_cast<const uint32_t*>(p);
-  } else if constexpr (NW == 2) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
-    w[0] = v.x; w[1] = v.y;
-  } else {
-#pragma unroll
-    for (int q = 0; q < NW / 4; ++q) {
-      const uint4 v = reinterpret_cast<const uint4*>(p)[q];
-      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-    }
-  }
-}
 template <int K, int S, int V>
 __device__ __forceinline__ void load_window_pair(const __nv_bfloat16* pa, const __nv_bfloat16* pb, const bool* lok,
                                                  const bool* rok, float2* xw) {
@@ -557,5 +677,6 @@ struct DArgs {
 };
 using DKernelFn = void (*)(DArgs);
 DKernelFn bwd_filter_kernel(int dtype, int S, int R, int V);
+DKernelFn bwd_filter_stream_kernel(int dtype, int S, int BR, int V);  // bf16 streaming (sdbf_kernel)
 }  // namespace direct
 }  // namespace dwk

@@ -230,6 +230,65 @@ static bool plan_direct_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p, int
   return p->max_chain <= 160 && groups * nsl < (int64_t)1 << 31;
 }
 
+// Streaming bf16 register-direct bwd_filter (sdbf_kernel) for K = 3, pad 1 on
+// planes whose rows split into L = Wo / V <= 32 lanes (MobileNet 112/56/28
+// columns): task = (image, band of BR dy rows); nps images per batch slice.
+static bool plan_stream_bwd_filter(const Geom& g, int num_sms, ChunkPlan* p, int V, int BR, int tps_arg) {
+  if (g.dtype != DWCONV_BF16 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
+  const int S = g.sh;
+  if (g.sw != S || (S != 1 && S != 2) || g.W != S * g.Wo || g.Wo % V != 0 || g.Wo / V > 32) return false;
+  if (!direct::bwd_filter_stream_kernel(g.dtype, S, BR, V)) return false;
+  const int L = (int)(g.Wo / V), SPW = 32 / L, spc = 8, P = SPW;
+  const int Co = (int)(g.C * g.m);
+  const int nsb = (int)((g.Ho + BR - 1) / BR);
+  const int64_t N = std::max<int64_t>(g.N, 1);
+  const int64_t groups = (Co + P - 1) / P;
+  const int64_t ntot = N * nsb;  // (image, band) tasks per channel, sliced into runs of tps
+  const int64_t nps = std::min<int64_t>(ntot, std::max(1, tps_arg));
+  const int64_t nsl = (ntot + nps - 1) / nps;
+  *p = ChunkPlan{};
+  p->direct = true;
+  p->dstream = BR;
+  p->threads = 256;
+  p->smem_bytes = 0;
+  p->R = BR; p->V = V; p->ri = 0;
+  p->P = P; p->nbands = 1; p->band_rows = (int)g.Ho; p->nsb = nsb; p->ncg = L;
+  p->dL = L; p->dSPW = SPW; p->dspc = spc;
+  p->groups = (int)groups; p->nslices = (int)nsl; p->n_per_slice = (int)nps; p->tpg = L;
+  p->grid = (int)(groups * nsl);
+  p->nchunks = p->grid;
+  const int64_t kmax = (nps + spc - 1) / spc;
+  p->max_chain = (int)(BR * V / 2 + 1 + kmax + L + spc + 2 * nchw::ilog2_ceil(nsl) + 1);
+  p->ws_bytes = two_level_ws_bytes(groups, nsl, Co);
+  return p->max_chain <= 160 && groups * nsl < (int64_t)1 << 31;
+}
+
+// Tasks per slice for the streaming variant: `res` resident CTAs per SM; picks the
+// slicing whose busiest SM (ceil(grid / SMs) CTAs of kmax set rounds each) is
+// closest to the even share, preferring <= `waves` CTAs per resident slot.
+static int stream_tps(const Geom& g, int num_sms, int V, int BR, int res, double waves) {
+  const int L = (int)(g.Wo / V);
+  if (L < 1 || L > 32) return 1;
+  const int P = 32 / L, spc = 8;
+  const int64_t groups = (g.C * g.m + P - 1) / P;
+  const int64_t ntot = std::max<int64_t>(g.N, 1) * ((g.Ho + BR - 1) / BR);
+  const double ideal = (double)groups * ntot / ((double)num_sms * spc);  // set rounds per SM, perfectly spread
+  double best = -1.0;
+  int64_t best_tps = ntot;
+  const int64_t cap = std::max<int64_t>(1, (int64_t)(waves * res * num_sms));
+  for (int64_t nsl = 1; nsl <= std::min<int64_t>(ntot, 128); ++nsl) {
+    const int64_t tps = (ntot + nsl - 1) / nsl;
+    const int64_t nsl2 = (ntot + tps - 1) / tps;
+    const int64_t grid = groups * nsl2;
+    if (grid > cap) break;
+    const int64_t kmax = (tps + spc - 1) / spc;
+    const double t = (double)((grid + num_sms - 1) / num_sms) * kmax;
+    const double sc = ideal / t;
+    if (sc > best + 1e-9) { best = sc; best_tps = tps; }
+  }
+  return (int)best_tps;
+}
+
 bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPlan* p,
                std::vector<ChunkPlan>* cands, int max_cands) {
   using namespace nchw;
@@ -274,6 +333,15 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     // padded staging needs 16-B aligned planes (full mode) or rows (band mode)
     const bool pad_full = (Hin * Win * eb) % 16 == 0;
     const bool pad_band = (Win * eb) % 16 == 0;
+    // bf16 3x3 stride-2 bwd_data with m = 1 runs the streaming polyphase strips (nchw_bwd_data.cu)
+    int bd_stream_vi = 0;
+    if (!fwd && S == 2 && K == 3 && m == 1 && g.dtype == DWCONV_BF16 && nchw::kBf16Interleave) {
+      for (int vi = 3; vi > 0 && !bd_stream_vi; --vi) {
+        const int64_t v = (int64_t)1 << vi;
+        if (g.W % (2 * v) == 0 && g.Wo % v == 0 && (vi < 3 || (g.Wo * eb) % 16 == 0)) bd_stream_vi = vi;
+      }
+    }
+    const bool bd_stream = bd_stream_vi > 0;
     const int out_rows_total = fwd ? (int)g.Ho : (int)g.H;
     p->ri = (out_rows_total % rows_for(pass, K, S, 0) == 0) ? 0 : 1;
     p->R = rows_for(pass, K, S, p->ri);
@@ -286,6 +354,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
         const int64_t tw = (int64_t)S << vi;
         if (g.W % tw == 0 && (g.W * eb) % std::min<int64_t>(16, tw * eb) == 0) { p->vi = vi; break; }
       }
+      if (bd_stream) p->vi = bd_stream_vi;  // bf16 3x3 m = 1: streaming strips of 2V dx columns
     }
     p->V = 1 << p->vi;
     p->ncg = fwd ? (int)(g.Wo / p->V) : (S == 1 ? (int)(g.W / p->V) : (int)((g.W + S * p->V - 1) / (S * p->V)));
@@ -356,7 +425,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
           if (P > Q) break;
           // bf16 fwd, whole planes, m = 1: plane-pair strips (half the tiles, each twice the work)
           static const bool pair_env = env_int("DWCONV_BF16_PAIR", 1, 0, 1) == 1;
-          p->pair = pair_env && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
+          p->pair = pair_env && !bd_stream && g.dtype == DWCONV_BF16 && K == 3 && m == 1 && P >= 2 &&
                     ((S * p->V) % 2 == 0) && kernel_for(pass, g.dtype, K, S, p->ri, p->vi, pad_full, true) != nullptr;
           const int64_t tiles = p->pair ? (P + 1) / 2 * tpp : P * tpp;
           const int64_t useful = p->pair ? (Q + 1) / 2 * tpp : Q * tpp;
@@ -533,12 +602,33 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     // variants of configs[2]: 1-2 MB per pass) one wave of CTAs leaves each with a few KB
     // and the cross-slice finalize dominates; the measured selection decides
     const size_t lead = std::min<size_t>(cands->size(), 4);
+    std::vector<ChunkPlan> var_bal, var_div;  // balanced slice counts go right behind the default
     for (size_t ci = 0; ci < lead; ++ci) {
-      for (int div : {2, 4, 8}) {
+      // slice counts: fewer (1/2, 1/4, 1/8), and the count whose busiest SM (ceil(grid / SMs)
+      // CTAs of nps images) comes closest to the even share within one / two waves of
+      // resident CTAs (a grid just past a wave leaves most SMs idle while the last CTAs run)
+      for (int div : {-1, -2, 2, 4, 8}) {
         ChunkPlan v = (*cands)[ci];
-        if (v.direct || v.small || v.nslices < 2 * div) continue;
+        if (v.direct || v.small) continue;
+        if (div > 0 && v.nslices < 2 * div) continue;
         const int64_t N = std::max<int64_t>(g.N, 1);
-        int64_t nsl = v.nslices / div;
+        int64_t nsl = div > 0 ? v.nslices / div : v.nslices;
+        if (div < 0) {
+          KernelFn fn = kernel_for(pass, g.dtype, K, S, v.ri, v.vi, v.padded);
+          const int occ = fn ? occupancy(fn, v.smem_bytes, v.threads) : 0;
+          if (occ < 1) continue;
+          const int64_t lo = std::max<int64_t>(1, (N * v.nbands + 31) / 32), hi = std::min<int64_t>(N, 128);
+          const double ideal = (double)v.groups * N / num_sms;
+          double best_sc = -1.0;
+          for (int64_t t = lo; t <= hi; ++t) {
+            const int64_t np_ = (N + t - 1) / t, ns_ = (N + np_ - 1) / np_;
+            const int64_t grid = (int64_t)v.groups * ns_;
+            if (grid > (int64_t)(-div) * occ * num_sms) break;
+            const double sc = ideal / ((double)((grid + num_sms - 1) / num_sms) * np_);
+            if (sc > best_sc + 1e-9) { best_sc = sc; nsl = ns_; }
+          }
+          if (nsl == v.nslices) continue;
+        }
         int64_t nps = (N + nsl - 1) / nps_guard(nsl);
         nsl = (N + nps - 1) / nps;
         if (nps * v.nbands > 32) continue;  // running-sum chain, as finalize()
@@ -550,22 +640,43 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
         v.max_chain = v.max_chain - (int)(old_nps * v.nbands) + (int)(nps * v.nbands) -
                       2 * ilog2_ceil(old_nsl) + 2 * ilog2_ceil(nsl);
         v.ws_bytes = two_level_ws_bytes(v.groups, nsl, g.C * m, KK);
-        if (v.max_chain > 160 || (int)cands->size() >= max_cands) continue;
+        if (v.max_chain > 160) continue;
         bool dup = false;
-        for (const ChunkPlan& o : *cands) dup = dup || (o.P == v.P && o.tpg == v.tpg && o.nbands == v.nbands &&
-                                                        o.band_rows == v.band_rows && o.nslices == v.nslices &&
-                                                        o.threads == v.threads && o.direct == v.direct);
-        if (!dup) cands->push_back(v);
+        auto same_v = [&](const ChunkPlan& o) {
+          return o.P == v.P && o.tpg == v.tpg && o.nbands == v.nbands && o.band_rows == v.band_rows &&
+                 o.nslices == v.nslices && o.threads == v.threads && o.direct == v.direct;
+        };
+        for (const ChunkPlan& o : *cands) dup = dup || same_v(o);
+        for (const ChunkPlan& o : var_bal) dup = dup || same_v(o);
+        for (const ChunkPlan& o : var_div) dup = dup || same_v(o);
+        if (!dup) (div < 0 ? var_bal : var_div).push_back(v);
       }
     }
+    const size_t at = std::min<size_t>(1, cands->size());
+    cands->insert(cands->begin() + at, var_bal.begin(), var_bal.end());
+    cands->insert(cands->end(), var_div.begin(), var_div.end());
     if (!fused) {  // register-direct variants (no smem staging) compete too
       for (int tasks : {2, 4}) {
         ChunkPlan d;
         if (plan_direct_bwd_filter(g, num_sms, &d, tasks, 4096)) cands->push_back(d);
       }
+      // bf16 streaming variants right behind the default (the list is capped)
+      std::vector<ChunkPlan> sv;
+      for (int V : {8, 4})
+        for (int BR : {16, 8})
+          for (double waves : {1.0, 3.0}) {
+            ChunkPlan d;
+            if (plan_stream_bwd_filter(g, num_sms, &d, V, BR, stream_tps(g, num_sms, V, BR, 2, waves))) {
+              bool dup = false;
+              for (const ChunkPlan& o : sv) dup = dup || (o.V == d.V && o.dstream == d.dstream && o.nslices == d.nslices);
+              if (!dup) sv.push_back(d);
+            }
+          }
+      cands->insert(cands->begin() + std::min<size_t>(1, cands->size()), sv.begin(), sv.end());
       ChunkPlan d0;  // the default planner's pick leads the list
       if (plan_direct_bwd_filter(g, num_sms, &d0)) cands->insert(cands->begin(), d0);
     }
+    if ((int)cands->size() > max_cands) cands->resize((size_t)max_cands);
   }
   return ok;
 }
@@ -705,7 +816,8 @@ cudaError_t launch_nchw_bwd_filter(const Geom& g, const ChunkPlan& p, const void
     const int64_t ebb = (g.dtype == DWCONV_F32) ? 4 : 2;
     d.pf = pf_env && (g.W * ebb) % 16 == 0 && (g.Wo * ebb) % 16 == 0 &&
            ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) & 15u) == 0;
-    direct::DKernelFn fn = direct::bwd_filter_kernel(g.dtype, g.sh, p.R, p.V);
+    direct::DKernelFn fn = p.dstream > 0 ? direct::bwd_filter_stream_kernel(g.dtype, g.sh, p.dstream, p.V)
+                                         : direct::bwd_filter_kernel(g.dtype, g.sh, p.R, p.V);
     static const bool pdl = nchw::env_int("DWCONV_PDL", 1, 0, 1) == 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)p.grid);

@@ -30,6 +30,9 @@ SETS = {
     # MobileNet-v1 layers at batch 128 (the >= 70 % target set): large planes and the 14x14 / 7x7 layers
     "mb128": [(128, 32, 112, 112, 1, 3, 1, 1), (128, 64, 112, 112, 1, 3, 2, 1), (128, 128, 56, 56, 1, 3, 1, 1),
               (128, 512, 14, 14, 1, 3, 1, 1), (128, 512, 14, 14, 1, 3, 2, 1), (128, 1024, 7, 7, 1, 3, 1, 1)],
+    # the same layers at batch 64 (configs[1], the fp32 headline)
+    "mb64": [(64, 32, 112, 112, 1, 3, 1, 1), (64, 64, 112, 112, 1, 3, 2, 1), (64, 128, 56, 56, 1, 3, 1, 1),
+             (64, 512, 14, 14, 1, 3, 1, 1), (64, 512, 14, 14, 1, 3, 2, 1), (64, 1024, 7, 7, 1, 3, 1, 1)],
     # the group-size sweep: stride-1 K = 3 / 5 / 7 on 56x56x128 (b64) and a MobileNet 3x3 layer (dw6, b128)
     "sweep": [(64, 128, 56, 56, 1, 3, 1, 1), (64, 128, 56, 56, 1, 5, 1, 2), (64, 128, 56, 56, 1, 7, 1, 3),
               (128, 128, 56, 56, 1, 3, 1, 1), (128, 512, 14, 14, 1, 3, 1, 1)],
@@ -114,7 +117,8 @@ def main():
                          pass_=pname, candidate=i, variant=var, S=S, CB=CB, us=us, gbs=nbytes / us / 1e3,
                          frac=nbytes / us / 1e3 / peak, useful_tfma=fma / us / 1e6,
                          mma_tflops=(2 * fma * S / us / 1e6) if S else None,
-                         grid=c["grid"] if c else None, block=c["block"] if c else None)
+                         grid=c["grid"] if c else None, block=c["block"] if c else None,
+                         family=c["kernel_family"] if c else None, slices=c["batch_slices"] if c else None)
                 rows.append(r)
                 print(json.dumps(r), flush=True)
             if cands[0] is not None:
