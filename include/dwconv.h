@@ -177,7 +177,8 @@ typedef struct {
   int64_t workspace_bytes;    /* bwd_filter workspace                                       */
   int32_t kernel_family;      /* NCHW chunk variant: 0 warp-specialised chunk, 1 small-plane
                                  warp tasks, 2 band bwd_filter, 3 register-direct bwd_filter,
-                                 4 streaming bf16 bwd_filter; 0 for other variants          */
+                                 4 streaming bf16 bwd_filter, 5 lane-per-plane (7x7/14x14);
+                                 0 for other variants                                       */
   int32_t reserved;
 } dwconv_plan_info;
 DWCONV_API int dwconv_plan(const dwconv_desc* d, int pass, dwconv_plan_info* info);

@@ -469,7 +469,7 @@ static void fill_info(const Geom& g, const Plan& p, int pass, dwconv_plan_info* 
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem_bytes; info->launches = 1;
     info->work_units = c.nchunks; info->planes_per_chunk = c.P; info->rows_per_band = c.band_rows;
     info->batch_slices = c.nslices; info->max_chain = c.max_chain; info->workspace_bytes = (int64_t)c.ws_bytes;
-    info->kernel_family = c.direct ? (c.dstream > 0 ? 4 : 3) : (c.small ? (c.sp.band ? 2 : 1) : 0);
+    info->kernel_family = c.direct ? (c.dstream > 0 ? 4 : 3) : (c.small ? (c.sp.lane ? 5 : c.sp.band ? 2 : 1) : 0);
   } else if (p.variant == DWCONV_VARIANT_NHWC_TMA) {
     const dwk::NhwcTmaPlan& c = p.tma;
     info->grid = c.grid; info->block = c.threads; info->smem_bytes = c.smem; info->launches = 1;
@@ -621,6 +621,16 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         if (dwk::band_chunk_plan(g, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2], sh[3])) cands.push_back(v);
       }
     }
+    if (pass <= DWCONV_PASS_BWD_FILTER) {
+      // lane-per-plane kernels (7x7 / 14x14, s1): {warps, ring slots}
+      static const int lshapes[][2] = {{4, 2}, {4, 3}, {8, 2}, {2, 3}, {2, 4}, {6, 2}, {8, 3}};
+      std::vector<ChunkPlan> lv;
+      for (const auto& sh : lshapes) {
+        ChunkPlan v;
+        if (dwk::lane_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1])) lv.push_back(v);
+      }
+      cands.insert(cands.begin() + std::min<size_t>(1, cands.size()), lv.begin(), lv.end());
+    }
     std::vector<ChunkPlan> more;
     ChunkPlan scratch;
     if (g.dtype == DWCONV_BF16 && pass <= DWCONV_PASS_BWD_FILTER) {
@@ -643,7 +653,7 @@ int dwconv_plan_candidates(const dwconv_desc* d, int pass, int max_candidates, d
         if (!dwk::small_chunk_plan(g, pass, di.sms, di.smem_optin, &v, sh[0], sh[1], sh[2])) continue;
         bool dup = false;
         for (const ChunkPlan& o : cands)
-          dup = dup || (o.small && !o.sp.pair && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices &&
+          dup = dup || (o.small && !o.sp.pair && !o.sp.lane && o.threads == v.threads && o.ns == v.ns && o.nslices == v.nslices &&
                         o.grid == v.grid);
         if (!dup) cands.push_back(v);
       }

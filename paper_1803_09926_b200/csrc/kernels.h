@@ -48,7 +48,11 @@ struct SmallPlan {
   // band bwd_filter for large planes (band_bf_kernel)
   bool band;
   int R, V, nbands, cpg, ppw;
+  bool lane;  // lane-per-plane kernels (lane_fd_kernel / lane_bf_kernel): 32-plane warp tasks
 };
+// lane-per-plane kernels (W = H in {7, 14}, s1): warps per CTA, ring slots per warp, batch slices (bwd_filter)
+bool plan_nchw_lane(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* plan, int warps, int stages,
+                    int slices = 0);
 bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* plan, int warps, int stages, int rows,
                        int ppw = 1);
 // warps / stages: CTA size and per-warp ring depth (0 = the defaults, env DWCONV_SMALL_WARPS / _STAGES)
@@ -107,6 +111,8 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
                std::vector<ChunkPlan>* cands = nullptr, int max_cands = 0);
 bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps = 0,
                       int stages = 0, int slices = 0, bool pair = false);
+bool lane_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* plan, int warps, int stages,
+                     int slices = 0);
 bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* plan, int warps, int stages, int rows,
                      int ppw = 1);
 cudaError_t launch_nchw_fwd(const Geom& g, const ChunkPlan& p, const void* x, const void* w, void* y,

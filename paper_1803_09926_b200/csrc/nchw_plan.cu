@@ -756,6 +756,28 @@ bool small_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, Chun
   return true;
 }
 
+bool lane_chunk_plan(const Geom& g, int pass, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages,
+                     int slices) {
+  SmallPlan sp;
+  if (!plan_nchw_lane(g, pass, num_sms, smem_optin, &sp, warps, stages, slices)) return false;
+  *p = ChunkPlan{};
+  p->small = true;
+  p->sp = sp;
+  p->threads = 32 * sp.warps;
+  p->grid = sp.grid;
+  p->smem_bytes = sp.smem;
+  p->P = 32;
+  p->nbands = 1;
+  p->band_rows = (int)g.H;
+  p->ns = sp.ns;
+  p->nchunks = (pass >= DWCONV_PASS_BWD_FILTER) ? (int64_t)sp.groups * sp.nslices : sp.ntasks;
+  p->groups = sp.groups;
+  p->nslices = sp.nslices;
+  p->n_per_slice = sp.nps;
+  p->max_chain = sp.max_chain;
+  p->ws_bytes = sp.ws_bytes;
+  return true;
+}
 bool band_chunk_plan(const Geom& g, int num_sms, int smem_optin, ChunkPlan* p, int warps, int stages, int rows,
                      int ppw) {
   SmallPlan sp;

@@ -1154,6 +1154,291 @@ __global__ void __launch_bounds__(256) band_bf_pair_kernel(const SArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- lane-per-plane kernels
+// W in {7, 14}, 3x3, stride 1, pad 1, m = 1.  A warp task is 32 consecutive planes
+// (one bulk copy); lane l computes plane l end to end -- no shuffles, no per-strip
+// index arithmetic -- with a 3-row window in registers and FFMA2 over interleaved
+// column pairs (u, u + H2), H2 = ceil(W / 2): the operand pair of tap j is
+// X2[u + j] = (xw[u + j], xw[u + j + H2]), xw = the row with its zero halo, so
+// bf16 values are widened straight into pair halves (PRMT / LOP3) and no pair is
+// formed by moves.  fwd / bwd_data write each output row back over the staged
+// input row (every input row is read into registers before the output row above
+// the next one is written), then lane 0 bulk-stores the 32 planes
+// (cp.async.bulk shared -> global) and refills the slot once the store has read it.
+// bwd_filter: CTA = (32 channels, batch slice), lane = channel; warps take the
+// slice's images in turn; the same windows with dy rows as the second operand.
+namespace lanek {
+template <class T, int W>
+struct Row {
+  static constexpr int H2 = (W + 1) / 2;
+  static constexpr int NP = H2 + 2;  // operand pairs per row
+  // raw words of one row: bf16 W even -> W/2 words; bf16 W odd -> W halfwords; fp32 -> W words
+  static constexpr int NR = (sizeof(T) == 2 && W % 2 == 0) ? W / 2 : W;
+  uint32_t r[NR];
+  __device__ __forceinline__ void load(const T* p) {
+    if constexpr (sizeof(T) == 2 && W % 2 == 0) {
+#pragma unroll
+      for (int q = 0; q < NR; ++q) r[q] = reinterpret_cast<const uint32_t*>(p)[q];
+    } else if constexpr (sizeof(T) == 2) {
+#pragma unroll
+      for (int q = 0; q < NR; ++q) r[q] = reinterpret_cast<const unsigned short*>(p)[q];
+    } else if constexpr (W % 2 == 0) {
+#pragma unroll
+      for (int q = 0; q < NR / 2; ++q) {
+        const uint2 v = reinterpret_cast<const uint2*>(p)[q];
+        r[2 * q] = v.x; r[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NR; ++q) r[q] = reinterpret_cast<const uint32_t*>(p)[q];
+    }
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) r[q] = 0u;
+  }
+  // element k of the row (0 <= k < W) as fp32
+  __device__ __forceinline__ float val(int k) const {
+    if constexpr (sizeof(T) == 2 && W % 2 == 0) return (k & 1) ? nchw::bfw_hi(r[k >> 1]) : nchw::bfw_lo(r[k >> 1]);
+    else if constexpr (sizeof(T) == 2) return nchw::bfw_lo(r[k]);
+    else return __uint_as_float(r[k]);
+  }
+  // xw[k]: the row with a zero column on each side (and zeros past it)
+  __device__ __forceinline__ float xw(int k) const { return (k >= 1 && k <= W) ? val(k - 1) : 0.f; }
+  __device__ __forceinline__ void pairs(float2* X2) const {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) X2[k] = make_float2(xw(k), xw(k + H2));
+  }
+  // D2[u] = (v[u], v[u + H2]) of the row itself (dy operand of bwd_filter)
+  __device__ __forceinline__ void dpairs(float2* D2) const {
+#pragma unroll
+    for (int u = 0; u < H2; ++u) D2[u] = make_float2(val(u), u + H2 < W ? val(u + H2) : 0.f);
+  }
+};
+// store W values o[c] = c < H2 ? acc[c].x : acc[c - H2].y at p
+template <class T, int W>
+__device__ __forceinline__ void store_row(T* p, const float2* acc) {
+  constexpr int H2 = (W + 1) / 2;
+  auto o = [&](int c) { return c < H2 ? acc[c].x : acc[c - H2].y; };
+  if constexpr (sizeof(T) == 2 && W % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < W / 2; ++q) reinterpret_cast<uint32_t*>(p)[q] = nchw::bf_pack(o(2 * q), o(2 * q + 1));
+  } else if constexpr (sizeof(T) == 2) {
+#pragma unroll
+    for (int c = 0; c < W; ++c) p[c] = __float2bfloat16_rn(o(c));
+  } else if constexpr (W % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < W / 2; ++q) reinterpret_cast<float2*>(p)[q] = make_float2(o(2 * q), o(2 * q + 1));
+  } else {
+#pragma unroll
+    for (int c = 0; c < W; ++c) reinterpret_cast<float*>(p)[c] = o(c);
+  }
+}
+}  // namespace lanek
+
+// MODE 0 fwd, 1 bwd_data (kernel rotated by 180 degrees: reading R9)
+template <class T, int W, int MODE>
+__global__ void __launch_bounds__(256) lane_fd_kernel(const SArgs a) {
+  using RowT = lanek::Row<T, W>;
+  constexpr int HW = W * W, H2 = RowT::H2, NP = RowT::NP;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const T* __restrict__ in = static_cast<const T*>(a.in);
+  T* __restrict__ out = static_cast<T*>(a.out);
+  const T* __restrict__ wt = static_cast<const T*>(a.w);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * nwarps;
+  constexpr uint32_t task_bytes = 32u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int64_t t, int s) {
+    if (t < a.ntasks) {
+      mbar_arrive_expect_tx(&bars[s], task_bytes);
+      bulk_g2s(slot(s), in + t * 32 * HW, task_bytes, &bars[s]);
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < a.ns; ++i) issue(gw + i * stride, i);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = gw; t < a.ntasks; t += stride) {
+    const int64_t q = t * 32 + lane;  // this lane's plane
+    const int c = (int)(q % a.C);
+    float wr[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wr[k] = Elem<T>::ldg(wt + (int64_t)c * 9 + (MODE == 1 ? 8 - k : k));
+    mbar_wait(&bars[s], ph);
+    T* pln = slot(s) + lane * HW;
+    // operand pairs of input rows oh - 1, oh, oh + 1 (each row widened once)
+    float2 X0[NP], X1[NP], X2[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) X0[k] = make_float2(0.f, 0.f);
+    {
+      RowT r;
+      r.load(pln);
+      r.pairs(X1);
+    }
+#pragma unroll
+    for (int oh = 0; oh < W; ++oh) {
+      if (oh + 1 < W) {
+        RowT r;
+        r.load(pln + (oh + 1) * W);
+        r.pairs(X2);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) X2[k] = make_float2(0.f, 0.f);
+      }
+      float2 acc[H2];
+#pragma unroll
+      for (int u = 0; u < H2; ++u) {
+        float2 v = __fmul2_rn(make_float2(wr[0], wr[0]), X0[u]);
+#pragma unroll
+        for (int j = 1; j < 3; ++j) v = __ffma2_rn(make_float2(wr[j], wr[j]), X0[u + j], v);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) v = __ffma2_rn(make_float2(wr[3 + j], wr[3 + j]), X1[u + j], v);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) v = __ffma2_rn(make_float2(wr[6 + j], wr[6 + j]), X2[u + j], v);
+        acc[u] = v;
+      }
+      lanek::store_row<T, W>(pln + oh * W, acc);  // rows <= oh + 1 are already in registers
+#pragma unroll
+      for (int k = 0; k < NP; ++k) { X0[k] = X1[k]; X1[k] = X2[k]; }
+    }
+    fence_proxy_async_smem();  // the generic-proxy stores, before the bulk copy reads them
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(out + t * 32 * HW, slot(s), task_bytes);
+      bulk_commit();
+      bulk_wait_read<0>();  // the slot has been read out: refill it
+      issue(t + a.ns * stride, s);
+    }
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  if (lane == 0) bulk_wait<0>();
+  griddep_launch_dependents();
+}
+
+// bwd_filter: CTA = (group of 32 channels, batch slice of nps images); warp w takes
+// images n0 + w, n0 + w + warps, ...; lane = channel.  Reduction, fixed order:
+// per image the window sums (W * H2 deep) -> a running sum over the warp's images
+// -> the warps in order -> per-slice partial -> two-level slice finalize.
+template <class T, int W>
+__global__ void __launch_bounds__(256) lane_bf_kernel(const SArgs a) {
+  using RowT = lanek::Row<T, W>;
+  constexpr int HW = W * W, H2 = RowT::H2, NP = RowT::NP;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * 8;
+  T* ring = reinterpret_cast<T*>(smem + 64 * nwarps + (size_t)warp * a.ns * a.slot_bytes);
+  const T* __restrict__ x = static_cast<const T*>(a.in);
+  const T* __restrict__ dy = static_cast<const T*>(a.in2);
+  const int g = blockIdx.x % a.groups;
+  const int sl = blockIdx.x / a.groups;
+  const int c0 = g * 32;
+  const int64_t n0 = (int64_t)sl * a.nps;
+  const int nimg = (int)(min((int64_t)a.N, n0 + a.nps) - n0);
+  if (lane == 0) {
+    for (int i = 0; i < a.ns; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  griddep_wait();
+  constexpr uint32_t half = 32u * HW * (uint32_t)sizeof(T);
+  auto slot = [&](int s) { return ring + (size_t)s * (a.slot_bytes / sizeof(T)); };
+  auto issue = [&](int k, int s) {  // k-th image of this warp
+    const int ni = warp + k * nwarps;
+    if (ni < nimg) {
+      const int64_t base = ((n0 + ni) * a.C + c0) * (int64_t)HW;
+      mbar_arrive_expect_tx(&bars[s], 2 * half);
+      bulk_g2s(slot(s), x + base, half, &bars[s]);
+      bulk_g2s(slot(s) + 32 * HW, dy + base, half, &bars[s]);
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < a.ns; ++i) issue(i, i);
+  float run[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) run[q] = 0.f;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int k = 0; warp + k * nwarps < nimg; ++k) {
+    mbar_wait(&bars[s], ph);
+    const T* px = slot(s) + lane * HW;
+    const T* pd = slot(s) + 32 * HW + lane * HW;
+    float2 loc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) loc[q] = make_float2(0.f, 0.f);
+    // x row ih meets dy rows ih + 1 (tap row 0), ih (1), ih - 1 (2)
+    float2 Dm[H2], D0[H2], Dp[H2];  // dy rows ih - 1, ih, ih + 1
+    {
+      RowT r;
+      r.load(pd);
+      r.dpairs(D0);
+#pragma unroll
+      for (int u = 0; u < H2; ++u) Dm[u] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int ih = 0; ih < W; ++ih) {
+      if (ih + 1 < W) {
+        RowT r;
+        r.load(pd + (ih + 1) * W);
+        r.dpairs(Dp);
+      }
+      RowT rx;
+      rx.load(px + ih * W);
+      float2 X[NP];
+      rx.pairs(X);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int u = 0; u < H2; ++u) {
+          if (ih + 1 < W) loc[0 * 3 + j] = __ffma2_rn(X[u + j], Dp[u], loc[0 * 3 + j]);
+          loc[1 * 3 + j] = __ffma2_rn(X[u + j], D0[u], loc[1 * 3 + j]);
+          if (ih >= 1) loc[2 * 3 + j] = __ffma2_rn(X[u + j], Dm[u], loc[2 * 3 + j]);
+        }
+#pragma unroll
+      for (int u = 0; u < H2; ++u) { Dm[u] = D0[u]; D0[u] = Dp[u]; }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) run[q] += loc[q].x + loc[q].y;
+    __syncwarp();
+    if (lane == 0) issue(k + a.ns, s);  // every lane is past the slot
+    if (++s == a.ns) { s = 0; ph ^= 1; }
+  }
+  griddep_launch_dependents();
+  // ---- reduce over the warps in order (ring slots are consumed: reuse the smem)
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem + 64 * nwarps);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) red[(warp * 32 + lane) * 9 + q] = run[q];
+  __syncthreads();
+  const int nch = min(32, a.C - c0);
+  float* part = a.ws_part + ((int64_t)sl * a.C + c0) * 9;
+  for (int e = threadIdx.x; e < nch * 9; e += blockDim.x) {
+    float v = red[e];
+    for (int w2 = 1; w2 < nwarps; ++w2) v += red[w2 * 32 * 9 + e];
+    part[e] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  {
+    const int ngrp = (a.nslices + 31) / 32;
+    nchw::finalize_two_level(a.ws_part, a.ws_part + (int64_t)a.nslices * a.C * 9, a.ws_ticket,
+                             a.ws_ticket + (int64_t)a.groups * ngrp, g, sl, a.nslices, (int64_t)a.C * 9,
+                             (int64_t)c0 * 9, nch * 9, a.dw, &s_last);
+  }
+}
+
 using SKernelFn = void (*)(SArgs);
 
 template <class T, int S, int R, int PPW>
@@ -1221,6 +1506,20 @@ SKernelFn pair_kernel_for(int pass, int W) {
                       : W == 28 ? small_fd_pair_kernel<28, 0> : nullptr;
   if (pass == 1) return W == 7 ? small_fd_pair_kernel<7, 1> : W == 14 ? small_fd_pair_kernel<14, 1>
                       : W == 28 ? small_fd_pair_kernel<28, 1> : nullptr;
+  return nullptr;
+}
+SKernelFn lane_kernel_for(int dtype, int pass, int W) {
+  using B = __nv_bfloat16;
+  if (W == 14) {
+    if (dtype == DWCONV_F32) return pass == 0 ? lane_fd_kernel<float, 14, 0> : pass == 1 ? lane_fd_kernel<float, 14, 1>
+                                  : pass == 2 ? lane_bf_kernel<float, 14> : nullptr;
+    return pass == 0 ? lane_fd_kernel<B, 14, 0> : pass == 1 ? lane_fd_kernel<B, 14, 1> : pass == 2 ? lane_bf_kernel<B, 14> : nullptr;
+  }
+  if (W == 7) {
+    if (dtype == DWCONV_F32) return pass == 0 ? lane_fd_kernel<float, 7, 0> : pass == 1 ? lane_fd_kernel<float, 7, 1>
+                                  : pass == 2 ? lane_bf_kernel<float, 7> : nullptr;
+    return pass == 0 ? lane_fd_kernel<B, 7, 0> : pass == 1 ? lane_fd_kernel<B, 7, 1> : pass == 2 ? lane_bf_kernel<B, 7> : nullptr;
+  }
   return nullptr;
 }
 SKernelFn kernel_for(int dtype, int pass, int W, int S = 1) {
@@ -1313,6 +1612,75 @@ bool plan_nchw_small(const Geom& g, int pass, int num_sms, int smem_optin, Small
   return p->max_chain <= 160;
 }
 
+// Lane-per-plane kernels: 32-plane warp tasks, W = H in {7, 14}, 3x3 s1 p1 m1, C % 32 == 0.
+bool plan_nchw_lane(const Geom& g, int pass, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages,
+                    int slices) {
+  using namespace small;
+  if (g.layout != DWCONV_NCHW || g.m != 1 || g.kh != 3 || g.kw != 3 || g.ph != 1 || g.pw != 1) return false;
+  if (g.sh != 1 || g.sw != 1 || g.H != g.W || (g.W != 7 && g.W != 14) || g.C % 32 != 0 || g.N < 1) return false;
+  if (pass > 2 || warps < 1 || warps > 8 || stages < 2 || stages > 6) return false;
+  if (g.N * g.C >= ((int64_t)1 << 31)) return false;
+  const int64_t eb = (g.dtype == DWCONV_F32) ? 4 : 2;
+  const int64_t plane = g.H * g.W * eb;
+  const bool bf = pass == 2;
+  *p = SmallPlan{};
+  p->lane = true;
+  p->S = 1;
+  p->warps = warps;
+  p->ns = stages;
+  p->slot_bytes = (uint32_t)(((bf ? 2 : 1) * 32 * plane + 15) & ~(int64_t)15);
+  p->smem = 64 * warps + warps * stages * (int)p->slot_bytes;
+  if (bf) p->smem = std::max(p->smem, 64 * warps + warps * 32 * 9 * 4);
+  if (p->smem > smem_optin - 1024) return false;
+  SKernelFn fn = lane_kernel_for(g.dtype, pass, (int)g.W);
+  if (!fn) return false;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - (int)fa.sharedSizeBytes) !=
+      cudaSuccess)
+    return false;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * warps, p->smem) != cudaSuccess || occ < 1)
+    return false;
+  p->occ = occ;
+  p->sms = num_sms;
+  if (!bf) {
+    p->ntasks = g.N * g.C / 32;
+    p->grid = (int)std::min<int64_t>((p->ntasks + warps - 1) / warps, (int64_t)occ * num_sms);
+    p->max_chain = 9;
+    return true;
+  }
+  // bwd_filter: groups of 32 channels x batch slices; the slice count whose busiest SM
+  // (ceil(grid / SMs) CTAs of ceil(nps / warps) images per warp) is closest to the even share
+  p->groups = (int)(g.C / 32);
+  const int64_t N = g.N;
+  int64_t nsl = 1;
+  if (slices > 0) {
+    nsl = std::min<int64_t>(slices, N);
+  } else {
+    double best = -1.0;
+    const double ideal = (double)p->groups * N / ((double)num_sms * warps);
+    for (int64_t t = 1; t <= std::min<int64_t>(N, 128); ++t) {
+      const int64_t np_ = (N + t - 1) / t, ns_ = (N + np_ - 1) / np_;
+      const int64_t grid = p->groups * ns_;
+      if (grid > 2 * (int64_t)occ * num_sms && t > 1) break;
+      const double sc = ideal / ((double)((grid + num_sms - 1) / num_sms) * ((np_ + warps - 1) / warps));
+      if (sc > best - 1e-9) { best = std::max(best, sc); nsl = ns_; }  // ties: more CTAs
+    }
+  }
+  int64_t nps = (N + nsl - 1) / nsl;
+  nsl = (N + nps - 1) / nps;
+  p->nslices = (int)nsl;
+  p->nps = (int)nps;
+  p->grid = (int)(p->groups * nsl);
+  int ls = 0;
+  while ((1ll << ls) < nsl) ++ls;
+  const int64_t H2 = (g.W + 1) / 2;
+  p->max_chain = (int)(g.W * H2 + (nps + warps - 1) / warps + warps + 2 * ls + 1);
+  p->ws_bytes = two_level_ws_bytes(p->groups, nsl, g.C);
+  return p->max_chain <= 160;
+}
+
 // Band bwd_filter for large planes (band_bf_kernel): Wo = 28 V, V in {1, 2, 4}.
 bool plan_nchw_band_bf(const Geom& g, int num_sms, int smem_optin, SmallPlan* p, int warps, int stages, int rows,
                        int ppw) {
@@ -1388,7 +1756,8 @@ cudaError_t launch_nchw_small(const Geom& g, const SmallPlan& p, int pass, const
     a.ws_ticket = static_cast<unsigned*>(ws);
     a.ws_part = reinterpret_cast<float*>(static_cast<char*>(ws) + tick);
   }
-  SKernelFn fn = p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R, p.ppw)
+  SKernelFn fn = p.lane ? lane_kernel_for(g.dtype, pass, (int)g.W)
+               : p.band ? band_kernel_for(g.dtype, (int)g.sh, p.V, p.R, p.ppw)
                : p.pair ? pair_kernel_for(pass, (int)g.W) : kernel_for(g.dtype, pass, (int)g.W, p.S);
   if (!fn) return cudaErrorInvalidValue;
   static const bool pdl = env_int("DWCONV_PDL", 1, 0, 1) == 1;
