@@ -83,6 +83,15 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
       if (it >= a.ns) mbar_wait(&empty[s], ph ^ 1);  // consumers released the stage
       const ChunkRows k = bd_rows<K, S>(a, c);
       const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
+      if constexpr (PADDED) {
+        if (a.nbands > 1 && k.hi == a.Ho) {  // zero rows under the last band's dy rows (read unchecked)
+          const StageSpec sp = spec_of(k);
+          for (int j = 0; j < m; ++j)
+            zero_bytes16(sin_of(s) + j * sp.pitch + sp.zbe + sp.cnt, (uint32_t)(PAD * Wo * sizeof(T) + 15) & ~15u,
+                         threadIdx.x, 32);
+          __syncwarp();
+        }
+      }
       if (threadIdx.x == 0) {
         const StageSpec sp = spec_of(k);
         const bool xb = stage_bulk_ok<T>(src_of(k), sp);  // else consumers copy this chunk themselves
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
       T* sin = sin_of(s);
       mbar_wait(&full[s], ph);
       const bool coop = !stage_bulk_ok<T>(src_of(k), sp);
-      const bool zbot = PADDED && a.nbands > 1 && k.hi == a.Ho;  // zero rows under the last band's dy rows
+      const bool zbot = false;  // the producer zeroes the rows under the last band's dy rows
       if (coop || zbot) {
         if (coop) stage_coop_n<T>(sin, src_of(k), sp, ctid, nct);
         if (zbot)

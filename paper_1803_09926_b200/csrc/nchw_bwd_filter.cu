@@ -98,6 +98,13 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   };
   auto issue = [&](int kk, int st) {
     const Rows r = rows_of(kk);
+    if constexpr (PADDED) {
+      if (a.nbands > 1 && r.hi == H) {  // zero rows under the last band of every plane (read unchecked)
+        const StageSpec xs = x_spec(r);
+        for (int pl = 0; pl < np; ++pl)
+          zero_bytes16(sx_of(st) + pl * xs.pitch + xs.zbe + xs.cnt, (uint32_t)(PAD * W * sizeof(T) + 15) & ~15u, 0, 1);
+      }
+    }
     if (chunk_bulk(r)) {
       const StageSpec xs = x_spec(r), ds = dy_spec(r);
       mbar_arrive_expect_tx(&bars[st], stage_bytes<T>(xs) + stage_bytes<T>(ds));
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     if (++st == a.ns) { st = 0; par ^= 1; }
     const StageSpec xs = x_spec(r);
     const bool bulk = chunk_bulk(r);
-    const bool zbot = PADDED && a.nbands > 1 && r.hi == H;
+    const bool zbot = false;  // issue() zeroes the rows under the last band of every plane
     if (!bulk || zbot) {  // uniform over the CTA
       if (!bulk) {
         stage_coop<T>(sx, x_src(r), xs);

@@ -285,6 +285,11 @@ template <class T>
 __device__ __forceinline__ void zero_elems(T* p, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = T(0.f);
 }
+// 16-B zero stores over [p, p + bytes) by thread t of nt (p and bytes 16-B multiples).
+__device__ __forceinline__ void zero_bytes16(void* p, uint32_t bytes, int t, int nt) {
+  uint4* q = reinterpret_cast<uint4*>(p);
+  for (uint32_t i = t; i < bytes / 16; i += nt) q[i] = make_uint4(0u, 0u, 0u, 0u);
+}
 // Same over a subset of threads (thread t of nt).
 template <class T>
 __device__ __forceinline__ void zero_elems_n(T* p, int n, int t, int nt) {

@@ -76,6 +76,13 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
       if (it >= a.ns) mbar_wait(&empty[s], ph ^ 1);  // consumers released the stage
       const ChunkRows k = fwd_rows<K, S>(a, c);
       const WeightWin ww = weight_win<T, KK>(a, k.q0, k.np);
+      if constexpr (PADDED) {
+        if (a.nbands > 1 && k.hi == a.H) {  // zero rows under the plane's last band (read unchecked)
+          const StageSpec sp = spec_of(k);
+          zero_bytes16(sin_of(s) + sp.zbe + sp.cnt, (uint32_t)(PAD * W * sizeof(T) + 15) & ~15u, threadIdx.x, 32);
+          __syncwarp();
+        }
+      }
       if (threadIdx.x == 0) {
         const T* src = x + (k.q0 * a.H + k.lo) * W;
         const StageSpec sp = spec_of(k);
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
       mbar_wait(&full[s], ph);
       const T* src = x + (k.q0 * a.H + k.lo) * W;
       const bool coop = !stage_bulk_ok<T>(src, sp);
-      const bool zbot = PADDED && a.nbands > 1 && k.hi == a.H;  // padding rows under the last band
+      const bool zbot = false;  // the producer zeroes the rows under a plane's last band
       if (coop || zbot) {  // uniform over the consumers
         if (coop) stage_coop_n<T>(sin, src, sp, ctid, nct);
         if (zbot) zero_elems_n(sin + sp.zbe + sp.cnt, PAD * W, ctid, nct);
