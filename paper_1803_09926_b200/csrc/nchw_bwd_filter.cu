@@ -23,7 +23,7 @@ namespace {
 // kernel (reading R9) -- and stores it, so dy is read from HBM once for both
 // gradients: 3|x| + 2|y| per layer instead of 3|x| + 3|y|.
 template <class T, int K, int S, int R, int V, bool PADDED, bool FUSED = false>
-__global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a) {
+__global__ void __launch_bounds__(kThreads + 32) nchw_bwd_filter_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int NRows = (R - 1) * S + K;
   // bf16, V >= 4: interleaved pairs (lanes = columns u, u + V/2; nchw_common.cuh), FFMA2 at any stride
@@ -46,12 +46,15 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   const int64_t n1 = min(a.N, n0 + a.nps);
   const int iters = (int)(n1 - n0) * a.nbands;
 
-  // empty[st]: every warp arrives after computing on stage st; thread 0 waits on it
-  // before refilling st, so warps never wait for each other inside the loop
+  // Warp-specialised: warp 0 is the producer (its lane 0 refills stage st once every
+  // consumer warp has arrived on empty[st]); warps 1.. compute.  Consumers never wait
+  // for each other inside the loop, and all ns stages stay in flight.
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 72);  // <= 7 stages below the zero row at 128
-  const int nwarps = (int)(blockDim.x >> 5);
+  const int ncw = (int)(blockDim.x >> 5) - 1;  // consumer warps
+  const int nct = 32 * ncw;
+  const int ctid = (int)threadIdx.x - 32;     // consumer thread index (< 0: producer warp)
   if (threadIdx.x == 0)
-    for (int i = 0; i < a.ns; ++i) mbar_init(&empty[i], nwarps);
+    for (int i = 0; i < a.ns; ++i) mbar_init(&empty[i], ncw);
   prologue(smem, bars, a);
   auto sx_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + 128 + st * a.in_stage); };
   auto sdy_of = [&](int st) { return reinterpret_cast<T*>(smem + a.in0_off + a.in2_off + st * a.in_stage); };
@@ -115,9 +118,9 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     }
   };
 
-  const int gp = threadIdx.x / a.tpg;  // dy plane of this thread within the group
-  const int lane_g = threadIdx.x - gp * a.tpg;
-  const bool active = gp < np * m;
+  const int gp = ctid >= 0 ? ctid / a.tpg : 0;  // dy plane of this thread within the group
+  const int lane_g = ctid - gp * a.tpg;
+  const bool active = ctid >= 0 && gp < np * m;
   const int ncg = (int)a.div_ncg.d;
   float run[KK];
 #pragma unroll
@@ -130,16 +133,22 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     for (int q = 0; q < KK; ++q) wf[q] = Elem<T>::ldg(wt + (int64_t)o * KK + (KK - 1 - q));
   }
 
-  if (threadIdx.x == 0)
-    for (int i = 0; i < a.ns - 1 && i < iters; ++i) issue(i, i);
+  if (ctid < 0) {
+    // ------------------------------------------------------------ producer warp
+    if (threadIdx.x == 0) {
+      int st = 0;
+      uint32_t par = 0;
+      for (int kk = 0; kk < iters; ++kk) {
+        if (kk >= a.ns) mbar_wait(&empty[st], par ^ 1);  // every consumer warp is done with the stage
+        issue(kk, st);
+        if (++st == a.ns) { st = 0; par ^= 1; }
+      }
+    }
+  } else {
+  // ------------------------------------------------------------ consumers
   int st = 0;
   uint32_t par = 0;
   for (int kk = 0; kk < iters; ++kk) {
-    if (threadIdx.x == 0 && kk + a.ns - 1 < iters) {
-      const int rs = (st == 0) ? a.ns - 1 : st - 1;  // the stage consumed in iteration kk - 1
-      if (kk >= 1) mbar_wait(&empty[rs], (uint32_t)(((kk - 1) / a.ns) & 1));
-      issue(kk + a.ns - 1, rs);
-    }
     const Rows r = rows_of(kk);
     const int cur = st;
     T* sx = sx_of(st);
@@ -149,14 +158,12 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     const StageSpec xs = x_spec(r);
     const bool bulk = chunk_bulk(r);
     const bool zbot = false;  // issue() zeroes the rows under the last band of every plane
-    if (!bulk || zbot) {  // uniform over the CTA
+    if (!bulk || zbot) {  // uniform over the consumers
       if (!bulk) {
-        stage_coop<T>(sx, x_src(r), xs);
-        stage_coop<T>(sdy, dy_src(r), dy_spec(r));
+        stage_coop_n<T>(sx, x_src(r), xs, ctid, nct);
+        stage_coop_n<T>(sdy, dy_src(r), dy_spec(r), ctid, nct);
       }
-      if (zbot)  // rows under the last band of every plane
-        for (int pl = 0; pl < np; ++pl) zero_elems(sx + pl * xs.pitch + xs.zbe + xs.cnt, PAD * W);
-      __syncthreads();
+      consumer_sync(nct);
     }
     if (active) {
       const int rows_x = r.hi - r.lo;
@@ -271,6 +278,7 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[cur]);  // this warp is done with the stage
   }
+  }
   __syncthreads();  // all warps are done with the stages before the sums are parked in them
 
   griddep_launch_dependents();
@@ -279,8 +287,9 @@ __global__ void __launch_bounds__(kThreads) nchw_bwd_filter_kernel(const NArgs a
   // (plane, tap) adds the tpg values -- a strided fixed-order sum per lane and a
   // fixed shuffle tree across lanes.
   float* red = reinterpret_cast<float*>(smem + a.in0_off);
+  if (ctid >= 0)
 #pragma unroll
-  for (int q = 0; q < KK; ++q) red[threadIdx.x * KK + q] = run[q];
+    for (int q = 0; q < KK; ++q) red[ctid * KK + q] = run[q];
   __syncthreads();
   const int Co = a.Co;
   float* part = a.ws_part + ((int64_t)sl * Co + (int64_t)c0ch * m) * KK;

@@ -522,7 +522,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     const int T = P * m * tpg;
     if (T > kThreads || T < 64 || T % 32 != 0) return;  // whole warps: the reduction shuffles full warps
     ChunkPlan c = *p;
-    c.threads = T; c.P = P; c.tpg = tpg; c.nbands = nb; c.band_rows = br;
+    c.threads = T + 32; c.P = P; c.tpg = tpg; c.nbands = nb; c.band_rows = br;  // + the producer warp
     c.in_bytes = round128(xb); c.in2_bytes = round128(dyb); c.out_bytes = 0;
     layout_smem(&c, g.W, eb, 0, ns);
     if (c.smem_bytes > max_smem_optin) layout_smem(&c, g.W, eb, 0, 2);
