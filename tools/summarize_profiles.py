@@ -79,15 +79,17 @@ def main():
     step = [("fwd", L) for L in layers] + [(p, L) for L in reversed(layers) for p in ("bwd_data", "bwd_filter")]
 
     launches = [l for l in read_launches(os.path.join(a.src, "launches.csv"))
-                if any(t in l["name"] for t in ("nchw_", "generic_", "dbf_kernel", "nhwc_", "small_", "band_"))]
+                if any(t in l["name"] for t in ("nchw_", "generic_", "dbf_kernel", "nhwc_", "small_", "band_", "lane_"))]
 
     def kind(name):
         import re as _re
-        m = _re.search(r"small_fd(?:_pair)?_kernel<[^>]*,\s*(\d)>", name)
-        if m:  # small-plane kernel: MODE 0 = fwd, 1 = bwd_data
+        m = _re.search(r"(?:small_fd(?:_pair)?|lane_fd)_kernel<[^>]*,\s*(\d)>", name)
+        if m:  # small-plane / lane-per-plane kernel: MODE 0 = fwd, 1 = bwd_data
             return "fwd" if m.group(1) == "0" else "bwd_data"
         if "small_fwd2_kernel" in name:
             return "fwd"
+        if "small_bd2_kernel" in name:
+            return "bwd_data"
         if "fwd_kernel" in name or "generic_fwd" in name:
             return "fwd"
         if "bwd_data" in name:
@@ -112,7 +114,7 @@ def main():
         dram = l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0)
         alg = (L.x_elems() + L.y_elems()) * eb + (L.w_elems() * eb if pas != "bwd_filter" else L.w_elems() * 4)
         import re
-        mm = re.search(r"(nchw_\w+_kernel|nhwc_\w+_kernel|small_\w+_kernel|band_\w+_kernel|dbf_kernel|generic_\w+)<([^>]*)>",
+        mm = re.search(r"(nchw_\w+_kernel|nhwc_\w+_kernel|small_\w+_kernel|band_\w+_kernel|lane_\w+_kernel|s?dbf_kernel|generic_\w+)<([^>]*)>",
                        l["name"])
         name = f"{mm.group(1)}<{mm.group(2)}>" if mm else l["name"][:40]
         md.append(f"| {i} | {L.name} | {pas} | {name} | {t_ns / 1e3:.2f} | {100 * t_ns / tot:.1f}% | {dram / 1e6:.1f} | "
