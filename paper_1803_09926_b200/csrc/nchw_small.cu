@@ -1665,7 +1665,7 @@ bool plan_nchw_lane(const Geom& g, int pass, int num_sms, int smem_optin, SmallP
       const int64_t grid = p->groups * ns_;
       if (grid > 2 * (int64_t)occ * num_sms && t > 1) break;
       const double sc = ideal / ((double)((grid + num_sms - 1) / num_sms) * ((np_ + warps - 1) / warps));
-      if (sc > best - 1e-9) { best = std::max(best, sc); nsl = ns_; }  // ties: more CTAs
+      if (sc > best + 1e-9) { best = sc; nsl = ns_; }  // ties: fewer CTAs (measured: the per-CTA reduction dominates)
     }
   }
   int64_t nps = (N + nsl - 1) / nsl;
