@@ -39,7 +39,9 @@ __device__ __forceinline__ ChunkRows bd_rows(const NArgs& a, int64_t c) {
 
 // PAIR (bf16, m = 1): tiles of two dx planes at once, FFMA2 lanes = planes --
 // S = 1 through stencil_strip_pair (flipped kernels), S = 2 polyphase.
-template <class T, int K, int S, int R, int V, bool PADDED, bool PAIR = false>
+// M1: compiled for m = 1 (the per-j partial then is the output strip itself: one
+// accumulator set instead of two -- 163 -> ~116 registers for bf16 3x3 s1 V = 8)
+template <class T, int K, int S, int R, int V, bool PADDED, bool PAIR = false, bool M1 = false>
 __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArgs a) {
   constexpr int PAD = (K - 1) / 2, KK = K * K;
   constexpr int D0 = floor_div(PAD - K + 1, S);
@@ -55,7 +57,7 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
   const T* __restrict__ dy = static_cast<const T*>(a.in);
   T* __restrict__ dx = static_cast<T*>(a.out);
   const T* __restrict__ wt = static_cast<const T*>(a.w);
-  const int W = a.W, Wo = a.Wo, m = a.m, H = a.H;
+  const int W = a.W, Wo = a.Wo, m = M1 ? 1 : a.m, H = a.H;
   const T* zrow = reinterpret_cast<const T*>(smem + a.zrow_off);
   const int nct = (int)blockDim.x - 32;  // consumer threads
 
@@ -417,22 +419,23 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
 }
 
 // V = 8 (one 16-B row load per window) exists for bf16 3x3 only.
-template <class T, int K, int S, int R, bool PD>
+template <class T, int K, int S, int R, bool PD, bool M1 = false>
 KernelFn v8_kernel() {
-  if constexpr (std::is_same<T, __nv_bfloat16>::value && K == 3 && PD) return nchw_bwd_data_kernel<T, K, S, R, 8, PD>;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value && K == 3 && PD)
+    return nchw_bwd_data_kernel<T, K, S, R, 8, PD, false, M1>;
   else return nullptr;
 }
 
-template <class T, int K, int S, bool PD>
+template <class T, int K, int S, bool PD, bool M1 = false>
 KernelFn pick_rv(int RI, int VI) {
   constexpr int R0 = rows_bd(K, S, 0), R1 = rows_bd(K, S, 1);
   if constexpr (S == 1) {
 #define DW_V(R)                                                   \
   switch (VI) {                                                   \
-    case 0: return nchw_bwd_data_kernel<T, K, S, R, 1, PD>;       \
-    case 1: return nchw_bwd_data_kernel<T, K, S, R, 2, PD>;       \
-    case 2: return PD ? nchw_bwd_data_kernel<T, K, S, R, 4, PD> : nullptr; \
-    case 3: return v8_kernel<T, K, S, R, PD>();                 \
+    case 0: return nchw_bwd_data_kernel<T, K, S, R, 1, PD, false, M1>;       \
+    case 1: return nchw_bwd_data_kernel<T, K, S, R, 2, PD, false, M1>;       \
+    case 2: return PD ? nchw_bwd_data_kernel<T, K, S, R, 4, PD, false, M1> : nullptr; \
+    case 3: return v8_kernel<T, K, S, R, PD, M1>();                 \
     default: return nullptr;                                      \
   }
     if (RI == 0) { DW_V(R0) } else { DW_V(R1) }
@@ -451,6 +454,15 @@ KernelFn pick_rv(int RI, int VI) {
       default: return nullptr;
     }
   }
+}
+
+template <class T, bool PD>
+KernelFn pick_t_m1(int K, int S, int RI, int VI) {  // stride 1, m = 1
+  if (S != 1) return nullptr;
+  if (K == 3) return pick_rv<T, 3, 1, PD, true>(RI, VI);
+  if (K == 5) return pick_rv<T, 5, 1, PD, true>(RI, VI);
+  if (K == 7) return pick_rv<T, 7, 1, PD, true>(RI, VI);
+  return nullptr;
 }
 
 template <class T, bool PD>
@@ -478,7 +490,11 @@ KernelFn pick_pair_v(int VI) {
   }
 }
 
-KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair) {
+KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair, bool m1) {
+  if (!pair && m1 && S == 1) {
+    if (dtype == DWCONV_F32) return padded ? pick_t_m1<float, true>(K, S, RI, VI) : pick_t_m1<float, false>(K, S, RI, VI);
+    return padded ? pick_t_m1<__nv_bfloat16, true>(K, S, RI, VI) : pick_t_m1<__nv_bfloat16, false>(K, S, RI, VI);
+  }
   if (pair) {
     if (dtype != DWCONV_BF16 || K != 3) return nullptr;
     if (S == 2) {  // polyphase pair tiles, 2V columns

@@ -57,7 +57,7 @@ using KernelFn = void (*)(NArgs);
 // RI: strip-height variant, VI: column-vector variant (V = 1 << VI).
 // PADDED: input planes staged with zero rows around them (see stage_issue).
 KernelFn fwd_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false);
-KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false);
+KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false, bool m1 = false);
 KernelFn bwd_filter_kernel(int dtype, int K, int S, int RI, int VI, bool padded);
 KernelFn bwd_fused_kernel(int dtype, int K, int S, int RI, int VI, bool padded);  // dx + dw in one pass
 

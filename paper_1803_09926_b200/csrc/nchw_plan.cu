@@ -87,9 +87,9 @@ int pick_vi(int64_t out_w, int64_t in_w, int S, int64_t eb, int K) {
   return 0;
 }
 
-KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false) {
+KernelFn kernel_for(int pass, int dtype, int K, int S, int RI, int VI, bool padded, bool pair = false, bool m1 = false) {
   if (pass == DWCONV_PASS_FWD) return fwd_kernel(dtype, K, S, RI, VI, padded, pair);
-  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded, pair);
+  if (pass == DWCONV_PASS_BWD_DATA) return bwd_data_kernel(dtype, K, S, RI, VI, padded, pair, m1);
   if (pass == kPassBwdFused) return bwd_fused_kernel(dtype, K, S, RI, VI, padded);
   return bwd_filter_kernel(dtype, K, S, RI, VI, padded);
 }
@@ -396,7 +396,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, nst);
       if (c.smem_bytes > max_smem_optin) layout_smem(&c, std::max(g.W, g.Wo), eb, (uint32_t)wb, 2);
       if (c.smem_bytes > max_smem_optin) return;
-      KernelFn kf = kernel_for(pass, g.dtype, K, S, c.ri, c.vi, c.padded, c.pair);
+      KernelFn kf = kernel_for(pass, g.dtype, K, S, c.ri, c.vi, c.padded, c.pair, g.m == 1);
       const int ctas = kf ? occupancy(kf, c.smem_bytes, c.threads) : 0;  // resident CTAs per SM
       if (ctas < 1) return;
       const int64_t grid = std::min<int64_t>(nch, (int64_t)ctas * num_sms);
@@ -469,7 +469,7 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
       c->nchunks = (c->nbands == 1) ? (Q + c->P - 1) / c->P : Q * c->nbands;
       if (c->nchunks >= ((int64_t)1 << 31)) return false;
       c->nsb = (c->band_rows + R - 1) / R;
-      KernelFn fn = kernel_for(pass, g.dtype, K, S, c->ri, c->vi, c->padded, c->pair);
+      KernelFn fn = kernel_for(pass, g.dtype, K, S, c->ri, c->vi, c->padded, c->pair, g.m == 1);
       if (!fn) return false;
       const int occ = occupancy(fn, c->smem_bytes, c->threads);
       if (occ < 1) return false;
@@ -478,7 +478,30 @@ bool plan_nchw(const Geom& g, int pass, int num_sms, int max_smem_optin, ChunkPl
     };
     *p = bestp;
     if (!finalize(p)) return false;
-    if (cands) collect_candidates(pool, p, finalize, cands, max_cands);
+    if (cands) {
+      collect_candidates(pool, p, finalize, cands, max_cands);
+      if (!fwd && S == 1 && m == 1) {
+        // stride-1 bwd_data is the forward stencil over dy (same staged shapes): the forward's
+        // leading shapes join the list, behind the default (the score-ranked list is capped
+        // and ranks the two passes' shapes differently; measured: bf16 dw2 fwd's 224-thread
+        // whole-plane shape is absent from the bwd_data list)
+        std::vector<ChunkPlan> fc;
+        ChunkPlan fd;
+        if (plan_nchw(g, DWCONV_PASS_FWD, num_sms, max_smem_optin, &fd, &fc, 12)) {
+          std::vector<ChunkPlan> add;
+          for (ChunkPlan c : fc) {
+            if (c.pair || !finalize(&c)) continue;
+            bool dup = false;
+            for (const ChunkPlan& o : *cands)
+              dup = dup || (o.P == c.P && o.nbands == c.nbands && o.band_rows == c.band_rows && o.threads == c.threads &&
+                            o.ns == c.ns && o.pair == c.pair);
+            if (!dup) add.push_back(c);
+          }
+          cands->insert(cands->begin() + std::min<size_t>(1, cands->size()), add.begin(), add.end());
+          if ((int)cands->size() > max_cands) cands->resize((size_t)max_cands);
+        }
+      }
+    }
     return true;
   }
 
@@ -817,7 +840,7 @@ cudaError_t launch_nchw_bwd_data(const Geom& g, const ChunkPlan& p, const void* 
   nchw::NArgs a = base_args(g, p);
   a.in = dy; a.w = w; a.out = dx;
   a.wbulk = weights_bulk_ok(g, w);
-  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded, p.pair);
+  nchw::KernelFn fn = nchw::bwd_data_kernel(g.dtype, g.kh, g.sh, p.ri, p.vi, p.padded, p.pair, g.m == 1);
   return launch(fn, p, st, a);
 }
 
