@@ -320,6 +320,25 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_data_kernel(const NArg
             continue;
           }
         }
+        if constexpr (M1 && S == 1 && std::is_same<T, __nv_bfloat16>::value && V >= 4 && kBf16Interleave) {
+          // bf16, m = 1: the flipped forward stencil with rows stored as they complete (3 live rows)
+          float wr[KK];
+          if (ww.tma) {
+#pragma unroll
+            for (int q = 0; q < KK; ++q) wr[q] = Elem<T>::load(swr + pp * KK + (KK - 1 - q));
+          } else {
+#pragma unroll
+            for (int q = 0; q < KK; ++q) wr[q] = swc[pp * KK + q];
+          }
+          T* xo = dx + (k.q0 + pp) * (int64_t)H * W + iw0;
+          stencil_strip_bf2_stream<K, 1, R, V, PADDED>(
+              reinterpret_cast<const __nv_bfloat16*>(sin + pp * sp.pitch + sp.zbe - k.lo * Wo),
+              reinterpret_cast<const __nv_bfloat16*>(zrow), Wo, k.lo, rows_dy, ih0 - PAD, iw0, wr,
+              [&](int tt, const float* v) {
+                if (ih0 + tt < k.r1) VecIO<T, V>::store(xo + (int64_t)(ih0 + tt) * W, v);
+              });
+          continue;
+        }
         if constexpr (!(kStream && V >= 8)) {
         float acc[R][TW];
 #pragma unroll

@@ -460,6 +460,60 @@ __device__ __forceinline__ void stencil_strip_bf2(const __nv_bfloat16* sp, const
     for (int u = 0; u < V / 2; ++u) { acc[tt][u] = acc2[tt][u].x; acc[tt][u + V / 2] = acc2[tt][u].y; }
 }
 
+// The same strip with each output row handed to store(tt, v[V]) as soon as its
+// last input row is in (row tt after input row tt*S + K - 1): only the K/S + 1 rows
+// still accumulating are live, not all R -- fewer registers, more warps per SM.
+template <int K, int S, int R, int V, bool PADDED, class StoreRow>
+__device__ __forceinline__ void stencil_strip_bf2_stream(const __nv_bfloat16* sp, const __nv_bfloat16* zp, int W,
+                                                         int lo, int rows, int ih0, int c0, const float* wr,
+                                                         StoreRow&& store) {
+  using Wd = Win<K, S, V>;
+  using W2 = Win2<K, S, V>;
+  constexpr int NRows = (R - 1) * S + K;
+  const int b0 = S * c0;
+  bool lok[Wd::NL > 0 ? Wd::NL : 1], rok[Wd::NR > 0 ? Wd::NR : 1];
+#pragma unroll
+  for (int l = 0; l < Wd::NL; ++l) lok[l] = b0 - Wd::NL + l >= 0;
+#pragma unroll
+  for (int r = 0; r < Wd::NR; ++r) rok[r] = b0 + Wd::NV + r < W;
+  float2 acc2[R][V / 2];
+#pragma unroll
+  for (int tt = 0; tt < R; ++tt)
+#pragma unroll
+    for (int u = 0; u < V / 2; ++u) acc2[tt][u] = make_float2(0.f, 0.f);
+  const __nv_bfloat16* prow = sp + ih0 * W + b0;
+#pragma unroll
+  for (int r = 0; r < NRows; ++r) {
+    const __nv_bfloat16* p;
+    if constexpr (PADDED) {
+      p = prow + r * W;
+    } else {
+      const bool rv = (unsigned)(ih0 + r - lo) < (unsigned)rows;
+      p = rv ? prow + r * W : zp + b0;
+    }
+    float2 X2[W2::NP];
+    load_window_bf2<K, S, V>(p, lok, rok, X2);
+#pragma unroll
+    for (int tt = 0; tt < R; ++tt) {
+      const int i = r - tt * S;
+      if (i >= 0 && i < K) {
+#pragma unroll
+        for (int jj = 0; jj < K; ++jj) {
+          const float w = wr[i * K + jj];
+#pragma unroll
+          for (int u = 0; u < V / 2; ++u) acc2[tt][u] = __ffma2_rn(make_float2(w, w), X2[S * u + jj], acc2[tt][u]);
+        }
+      }
+      if (r == tt * S + K - 1) {
+        float v[V];
+#pragma unroll
+        for (int u = 0; u < V / 2; ++u) { v[u] = acc2[tt][u].x; v[u + V / 2] = acc2[tt][u].y; }
+        store(tt, v);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ stencil strip
 // acc[tt][u] = sum_{i,jj} wr[i*K+jj] * X[oh0*S - PAD + tt*S + i][S*(c0+u) - PAD + jj]
 // where input row ih lives at sp + ih*W.  PADDED: every row the strip touches is

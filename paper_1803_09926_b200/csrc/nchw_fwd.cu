@@ -198,6 +198,17 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
 #pragma unroll
           for (int q = 0; q < KK; ++q) wr[q] = swc[pp * KK + q];
         }
+        T* yo = y + ((k.q0 * m + pp) * a.Ho + oh0) * Wo + c0;
+        if constexpr (std::is_same<T, __nv_bfloat16>::value && S == 1 && V >= 4 && kBf16Interleave) {
+          // bf16 stride 1: rows leave as soon as they are complete (3 live rows instead of R;
+          // measured slower at stride 2, which keeps the whole strip)
+          stencil_strip_bf2_stream<K, S, R, V, PADDED>(
+              reinterpret_cast<const __nv_bfloat16*>(sin + pin * sp.pitch + sp.zbe - k.lo * W),
+              reinterpret_cast<const __nv_bfloat16*>(zrow), W, k.lo, rows_in, oh0 * S - PAD, c0, wr,
+              [&](int tt, const float* v) {
+                if (oh0 + tt < k.r1) VecIO<T, V>::store(yo + tt * Wo, v);
+              });
+        } else {
         float acc[R][V];
 #pragma unroll
         for (int tt = 0; tt < R; ++tt)
@@ -205,10 +216,10 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_fwd_kernel(const NArgs a) 
           for (int u = 0; u < V; ++u) acc[tt][u] = 0.f;
         stencil_strip<T, K, S, R, V, PADDED>(sin + pin * sp.pitch + sp.zbe - k.lo * W, zrow, W, k.lo, rows_in,
                                              oh0 * S - PAD, c0, wr, acc);
-        T* yo = y + ((k.q0 * m + pp) * a.Ho + oh0) * Wo + c0;
 #pragma unroll
         for (int tt = 0; tt < R; ++tt)
           if (oh0 + tt < k.r1) VecIO<T, V>::store(yo + tt * Wo, acc[tt]);
+        }
       }
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
