@@ -461,14 +461,14 @@ KernelFn pick_rv(int RI, int VI) {
 #undef DW_V
   } else {  // stride 2: tiles of R rows x 2V columns
     switch (VI) {
-      case 0: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 1, PD> : nchw_bwd_data_kernel<T, K, S, R1, 1, PD>;
-      case 1: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 2, PD> : nchw_bwd_data_kernel<T, K, S, R1, 2, PD>;
+      case 0: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 1, PD, false, M1> : nchw_bwd_data_kernel<T, K, S, R1, 1, PD, false, M1>;
+      case 1: return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 2, PD, false, M1> : nchw_bwd_data_kernel<T, K, S, R1, 2, PD, false, M1>;
       case 2:
-        if constexpr (K == 3) return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 4, PD> : nchw_bwd_data_kernel<T, K, S, R1, 4, PD>;
+        if constexpr (K == 3) return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 4, PD, false, M1> : nchw_bwd_data_kernel<T, K, S, R1, 4, PD, false, M1>;
         else return nullptr;
       case 3:  // bf16 3x3 streaming strips (m = 1), 16 dx columns
         if constexpr (K == 3 && PD && std::is_same<T, __nv_bfloat16>::value)
-          return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 8, PD> : nchw_bwd_data_kernel<T, K, S, R1, 8, PD>;
+          return RI == 0 ? nchw_bwd_data_kernel<T, K, S, R0, 8, PD, false, M1> : nchw_bwd_data_kernel<T, K, S, R1, 8, PD, false, M1>;
         else return nullptr;
       default: return nullptr;
     }
@@ -476,11 +476,16 @@ KernelFn pick_rv(int RI, int VI) {
 }
 
 template <class T, bool PD>
-KernelFn pick_t_m1(int K, int S, int RI, int VI) {  // stride 1, m = 1
-  if (S != 1) return nullptr;
-  if (K == 3) return pick_rv<T, 3, 1, PD, true>(RI, VI);
-  if (K == 5) return pick_rv<T, 5, 1, PD, true>(RI, VI);
-  if (K == 7) return pick_rv<T, 7, 1, PD, true>(RI, VI);
+KernelFn pick_t_m1(int K, int S, int RI, int VI) {  // m = 1
+  if (S == 1) {
+    if (K == 3) return pick_rv<T, 3, 1, PD, true>(RI, VI);
+    if (K == 5) return pick_rv<T, 5, 1, PD, true>(RI, VI);
+    if (K == 7) return pick_rv<T, 7, 1, PD, true>(RI, VI);
+  } else if (S == 2) {
+    if (K == 3) return pick_rv<T, 3, 2, PD, true>(RI, VI);
+    if (K == 5) return pick_rv<T, 5, 2, PD, true>(RI, VI);
+    if (K == 7) return pick_rv<T, 7, 2, PD, true>(RI, VI);
+  }
   return nullptr;
 }
 
@@ -510,7 +515,7 @@ KernelFn pick_pair_v(int VI) {
 }
 
 KernelFn bwd_data_kernel(int dtype, int K, int S, int RI, int VI, bool padded, bool pair, bool m1) {
-  if (!pair && m1 && S == 1) {
+  if (!pair && m1 && (S == 1 || S == 2)) {
     if (dtype == DWCONV_F32) return padded ? pick_t_m1<float, true>(K, S, RI, VI) : pick_t_m1<float, false>(K, S, RI, VI);
     return padded ? pick_t_m1<__nv_bfloat16, true>(K, S, RI, VI) : pick_t_m1<__nv_bfloat16, false>(K, S, RI, VI);
   }
