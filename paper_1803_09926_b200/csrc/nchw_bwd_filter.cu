@@ -222,18 +222,21 @@ __global__ void __launch_bounds__(kThreads + 32) nchw_bwd_filter_kernel(const NA
             }
           }
         } else {
+        // dy row tt is loaded at its first use (input row tt*S): at most K/S + 1 rows live
         float dv[R][V];
 #pragma unroll
-        for (int tt = 0; tt < R; ++tt) {
-          if (oh0 + tt < r.r1) {
-            VecIO<T, V>::load(s_dy + (oh0 + tt) * Wo + c0, dv[tt]);
-          } else {
-#pragma unroll
-            for (int u = 0; u < V; ++u) dv[tt][u] = 0.f;
-          }
-        }
-#pragma unroll
         for (int rr = 0; rr < NRows; ++rr) {
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt) {
+            if (rr == tt * S) {
+              if (oh0 + tt < r.r1) {
+                VecIO<T, V>::load(s_dy + (oh0 + tt) * Wo + c0, dv[tt]);
+              } else {
+#pragma unroll
+                for (int u = 0; u < V; ++u) dv[tt][u] = 0.f;
+              }
+            }
+          }
           const int ih = ih0 + rr;
           const bool rv = PADDED || (unsigned)(ih - r.lo) < (unsigned)rows_x;
           const T* p = (rv ? s_x + ih * W : zrow) + b0;
