@@ -24,6 +24,11 @@ CASES = [  # name, (N, C, H, W, m, K, s, p), layout, dtype
     ("small14", (4, 32, 14, 14, 1, 3, 1, 1), NCHW, "f32"),
     ("small7_bf16", (4, 64, 7, 7, 1, 3, 1, 1), NCHW, "bf16"),
     ("band112", (2, 8, 112, 112, 1, 3, 1, 1), NCHW, "f32"),
+    # round 3: bf16 interleaved strips, producer-warp bwd_filter, streaming bwd_filter and s2 bwd_data, m = 1 kernels
+    ("bf16_112", (2, 32, 112, 112, 1, 3, 1, 1), NCHW, "bf16"),
+    ("bf16_112_s2", (2, 32, 112, 112, 1, 3, 2, 1), NCHW, "bf16"),
+    # round 3: lane-per-plane kernels (C % 32 == 0)
+    ("lane14_bf16", (4, 64, 14, 14, 1, 3, 1, 1), NCHW, "bf16"),
     ("band56_s2", (2, 16, 56, 56, 1, 3, 2, 1), NCHW, "f32"),
     ("nhwc_tma_s1", (2, 64, 28, 28, 1, 3, 1, 1), NHWC, "f32"),
     ("nhwc_tma_s2_bf16", (2, 128, 28, 28, 1, 3, 2, 1), NHWC, "bf16"),
