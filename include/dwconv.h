@@ -59,7 +59,10 @@
 extern "C" {
 #endif
 
-#define DWCONV_ABI_VERSION 1
+/* 2 (round 3): dwconv_plan_info grew kernel_family (+ reserved), DWCONV_MAX_CANDIDATES 32 -> 48,
+   DWCONV_VARIANT values unchanged.  A caller built against version 1 passes a smaller
+   dwconv_plan_info and must not be linked against this library. */
+#define DWCONV_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define DWCONV_API __attribute__((visibility("default")))

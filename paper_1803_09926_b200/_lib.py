@@ -95,7 +95,7 @@ def load() -> ctypes.CDLL:
               "dwconv_workspace_init", "dwconv_plan", "dwconv_plan_candidates", "dwconv_plan_select",
               "dwconv_set_variant_override"):
         getattr(lib, f).restype = i32
-    if lib.dwconv_abi_version() != 1:
+    if lib.dwconv_abi_version() != 2:
         raise RuntimeError("libdwconv ABI version mismatch")
     _lib = lib
     return lib

@@ -32,7 +32,7 @@ def test_every_declared_symbol_is_exported(lib):
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_declared()) == set(_lib.FUNCTIONS)
-    assert lib.dwconv_abi_version() == 1
+    assert lib.dwconv_abi_version() == 2
 
 
 def test_product_does_not_import_oracle():
