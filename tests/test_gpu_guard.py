@@ -91,3 +91,23 @@ def test_guard_bands_every_candidate(shape, dtype):
                 assert np.all(wb[:PAD] == 0x5A) and np.all(wb[PAD + wsb:] == 0x5A), f"{tag}: workspace overrun"
                 assert np.all(wb[PAD:PAD + wsb] == 0), f"{tag}: workspace not handed back zeroed"
                 assert np.array_equal(dwt.view(C * m, K, K).cpu().numpy().astype(f64), ref_dw), tag
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("dtype,batch", [("f32", 64), ("bf16", 128)])
+def test_candidate_lists_capped(dtype, batch, layout):
+    """Every MobileNet layer's candidate list (count query with max_candidates = 0 included) stays within
+    DWCONV_MAX_CANDIDATES, and every listed index builds a plan handle (include/dwconv.h)."""
+    from paper_1803_09926_b200 import _lib
+    import ctypes
+    lib = _lib.load()
+    for L in synth.mobilenet_v1_dw(batch):
+        d = ops.make_desc(L.n, L.c, L.h, L.w, L.m, L.k, L.s, L.p, layout, F32 if dtype == "f32" else BF16)
+        for pas in (0, 1, 2):
+            count = ctypes.c_int(-1)
+            rc = lib.dwconv_plan_candidates(ctypes.byref(d), pas, 0, None, ctypes.byref(count))
+            assert rc == 0 and 0 <= count.value <= _lib.MAX_CANDIDATES, (L.name, pas, count.value)
+            cands = ops.dwconv_plan_candidates(d, pas)
+            assert len(cands) == count.value
+            for i in range(len(cands)):
+                ops.Plan(d, pas, i)
